@@ -1,0 +1,192 @@
+/*
+ * mri_b200.h -- C-ABI of the B200-native MRI slow step (libmri_b200.so).
+ *
+ * Drop-in boundary for the data-parallel work inside one explicit MRI-GARK
+ * slow step of the reference multirate toolkit.  Every entry point replaces a
+ * reference interface, cited as proj/<file>:<line> under /root/reference:
+ *
+ *   mr_mri_step / mr_mri_integrate   <- multirate::mri_step / mri_integrate
+ *                                       (include/multirate/mri.hpp:117-133,
+ *                                        src/mri.cpp:323-435, :524-540)
+ *   mr_coupling_load                 <- MriCoupling + finalize()/import_coupling
+ *                                       (mri.hpp:32-62, mri.cpp:59-167, :590-626)
+ *   mr_table_load                    <- ButcherTable (butcher.hpp:16-27) used by
+ *                                       erk_step (erk.cpp:9-38)
+ *   mr_fast_* / mr_slow_*            <- PartitionedSystem::f_fast / f_explicit
+ *                                       (partitioned_system.hpp:25-61); the RHS
+ *                                       callbacks become device "plugins"
+ *   mr_fast_rhs / mr_slow_rhs        <- one RhsFn call (partitioned_system.hpp:17)
+ *   mr_wrms_norm ... mr_all_finite   <- state_vector.hpp:119-176
+ *   status codes                     <- ContractError / IntegrationError
+ *                                       (state_vector.hpp:22-36)
+ *
+ * Conventions: plain pointers and sizes, no exceptions across the ABI, no
+ * torch types.  Host state buffers use exactly the reference's species-major
+ * layout Y[comp * ncell + cell], cell = (i * n1 + j) * n2 + k (axis 2
+ * fastest), so a multirate::StateVector::data() can be passed directly.
+ * Counters are uint64_t[8] in EvalCounters field order
+ * (partitioned_system.hpp:66-79) and are ACCUMULATED like the reference's
+ * by-reference EvalCounters.  Functions are synchronous on the context's
+ * stream unless stated otherwise.
+ */
+#ifndef MRI_B200_H_
+#define MRI_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mr_ctx mr_ctx;
+
+/* status codes */
+#define MR_OK 0
+#define MR_CONTRACT 1    /* multirate::ContractError */
+#define MR_INTEGRATION 2 /* multirate::IntegrationError (see fail_stage) */
+#define MR_CUDA 3        /* CUDA / NCCL failure */
+
+/* StageKind (mri.hpp:23) */
+#define MR_STAGE_FAST_IVP 0
+#define MR_STAGE_IMPLICIT_SOLVE 1
+#define MR_STAGE_EXPLICIT_UPDATE 2
+
+/* counters index (EvalCounters field order) */
+#define MR_CNT_FAST_EVALS 0
+#define MR_CNT_IMPLICIT_EVALS 1
+#define MR_CNT_EXPLICIT_EVALS 2
+#define MR_CNT_IMPLICIT_SOLVES 3
+#define MR_CNT_NONLINEAR_ITERS 4
+#define MR_CNT_LINEAR_ITERS 5
+#define MR_CNT_PRECOND_SOLVES 6
+#define MR_CNT_FAST_IVPS 7
+
+/* ---------------- context / grid ---------------- */
+int mr_ctx_create(int device, mr_ctx** out);
+void mr_ctx_destroy(mr_ctx* ctx);
+const char* mr_last_error(const mr_ctx* ctx);
+int mr_version(void);
+
+/* Grid of n0 x n1 x n2 global cells with n_comp components per cell.  This
+ * context owns the slab of planes [i0, i0 + n0_local) along axis 0 (the
+ * slowest axis); a single-GPU run passes i0 = 0, n0_local = n0. */
+int mr_grid_set(mr_ctx* ctx, int n0, int n1, int n2, int n_comp, double length,
+                int i0, int n0_local);
+
+/* ---------------- method data ---------------- */
+/* Raw coupling tables as in the v1 audit format (mri.cpp:560-626): c[s],
+ * kind[s], gamma[n_deg][s][s], omega[n_deg][s][s].  Validated and finalized
+ * with the reference's rules (mri.cpp:59-167). */
+int mr_coupling_load(mr_ctx* ctx, int s, int n_deg, const double* c, const int* kind,
+                     const double* gamma, const double* omega);
+/* Same, from the reference's v1 text (export_coupling output). */
+int mr_coupling_load_text(mr_ctx* ctx, const char* text);
+/* Explicit inner table A[s][s], b[s], c[s] (s <= 6). */
+int mr_table_load(mr_ctx* ctx, int s, const double* A, const double* b, const double* c);
+/* MriMethodConfig::m (mri.hpp:64-68) */
+int mr_set_substeps(mr_ctx* ctx, int m);
+
+/* ---------------- physics plugins (PartitionedSystem) ---------------- */
+/* fast = per-cell Arrhenius chemistry (n_comp must be S + 1, energy last).
+ * species[S*5] = {W, a, b, h0, s0}; reactions[R*3] = {lnA, beta, Ea/Rc};
+ * rspecies[R*4] = {r1, r2, p1, p2} (-1 = absent).  DESIGN.md "Physics". */
+int mr_fast_chemistry(mr_ctx* ctx, int S, int R, double rho, const double* species,
+                      const double* reactions, const int* rspecies);
+/* fast = per-cell linear map f = A v, A[n_comp][n_comp] (test plugin; the
+ * reference's LinearTwoRateOde, models.cpp:47-63, applied per cell) */
+int mr_fast_linear(mr_ctx* ctx, const double* A);
+int mr_fast_none(mr_ctx* ctx); /* f_fast absent */
+/* slow = 3D periodic centred advection-diffusion, order 2/4/8.  vel_prof ==
+ * NULL: uniform velocity u[3]; else tabulated profiles [3][2][nmax] with
+ * u_d = P[d][0][coord of lower other axis] + P[d][1][coord of upper one]. */
+int mr_slow_stencil(mr_ctx* ctx, int order, double diffusion, const double* u,
+                    const double* vel_prof, int nmax);
+int mr_slow_linear(mr_ctx* ctx, const double* A);
+int mr_slow_none(mr_ctx* ctx);
+
+/* ---------------- state ---------------- */
+int mr_state_upload(mr_ctx* ctx, const double* host);   /* local slab, species-major */
+int mr_state_download(mr_ctx* ctx, double* host);
+/* device pointer of the current state (valid until the next step) */
+double* mr_state_device_ptr(mr_ctx* ctx);
+size_t mr_state_dof(const mr_ctx* ctx);
+
+/* ---------------- stepping ---------------- */
+/* One slow step t -> t+H of the device-resident state.  On MR_INTEGRATION the
+ * state is unchanged and *fail_stage is the reference's
+ * IntegrationError::stage_index (inner ERK stage index for a fast-IVP
+ * failure, MRI stage index otherwise); counters then hold the reference's
+ * partial counts up to the failure. */
+int mr_mri_step(mr_ctx* ctx, double t, double H, uint64_t* counters, int* fail_stage);
+int mr_mri_integrate(mr_ctx* ctx, double t0, double tf, double H, uint64_t* counters,
+                     int* fail_stage);
+/* End-to-end variant with HOST buffers: H2D of y_in, the step, D2H of y_out. */
+int mr_mri_step_host(mr_ctx* ctx, double t, double H, const double* y_in, double* y_out,
+                     uint64_t* counters, int* fail_stage);
+/* Location of the last failure: MRI stage, fast substep, inner stage. */
+int mr_last_failure(const mr_ctx* ctx, int* mri_stage, int* substep, int* inner_stage);
+
+/* Single RHS evaluations ("Mode A": a reference RhsFn backed by the GPU).
+ * Host buffers, local slab; slow evaluation exchanges halos when sharded. */
+int mr_fast_rhs(mr_ctx* ctx, double t, const double* y, double* out);
+int mr_slow_rhs(mr_ctx* ctx, double t, const double* y, double* out);
+
+/* ---------------- reductions (device pointers, this context's stream) ---------------- */
+int mr_wrms_norm(mr_ctx* ctx, const double* x, const double* w, size_t n, double* out);
+int mr_two_norm(mr_ctx* ctx, const double* x, size_t n, double* out);
+int mr_dot(mr_ctx* ctx, const double* x, const double* y, size_t n, double* out);
+int mr_max_norm(mr_ctx* ctx, const double* x, size_t n, double* out);
+int mr_max_norm_component(mr_ctx* ctx, const double* x, size_t n, size_t offset,
+                          size_t count, double* out);
+int mr_all_finite(mr_ctx* ctx, const double* x, size_t n, int* out);
+
+/* ---------------- multi-GPU (slab decomposition over NCCL) ---------------- */
+int mr_nccl_unique_id(char* id128);
+int mr_comm_init(mr_ctx* ctx, int nranks, int rank, const char* id128);
+
+/* In-process "virtual ranks" (one GPU, several slab contexts sharing the
+ * device): the same slab code path with halos copied device-to-device. */
+int mr_group_step(mr_ctx** ctxs, int n, double t, double H, uint64_t* counters,
+                  int* fail_stage);
+
+/* ---------------- host-side generators (seeded, bit-reproducible) ---------------- */
+int mr_mechanism_generate(uint64_t seed, int S, int R, double* species, double* reactions,
+                          int* rspecies);
+/* initial condition of the local slab [i0, i0+n0_local) of an n0 x n1 x n2 grid */
+int mr_initial_condition(uint64_t seed, int S, double rho, const double* species, int n0,
+                         int n1, int n2, double length, int i0, int n0_local, double* Y,
+                         int threads);
+int mr_velocity_profiles(uint64_t seed, int n0, int n1, int n2, double length, double* prof);
+
+/* ---------------- host-only method inspection (no GPU needed) ---------------- */
+/* Parse + finalize a v1 coupling text with the reference's rules; fills the
+ * stage count, kinds, slow-evaluation schedule and substeps per stage for m.
+ * Returns MR_CONTRACT with the reference's message in err on violation. */
+int mr_coupling_inspect(const char* text, int m, int* s, int* kinds, int* eval_at, int* n_sub,
+                        char* err, size_t errlen);
+/* EvalCounters increments of one successful slow step (plan of the device
+ * stage loop) for an inner table of s_f stages. */
+int mr_step_counts(const char* text, int s_f, int m, int fast_present, int slow_present,
+                   uint64_t* counters, char* err, size_t errlen);
+
+/* ---------------- instrumentation ---------------- */
+/* cudaStream_t of the context (for event timing by the caller) */
+void* mr_stream(mr_ctx* ctx);
+/* number of kernels this context launched since creation */
+uint64_t mr_launch_count(const mr_ctx* ctx);
+/* fp64 work accounting of one chemistry RHS evaluation */
+double mr_chem_flops_per_eval(const mr_ctx* ctx);
+/* measured fp64 FMA peak of this GPU (DFMA chain microbenchmark), TFLOP/s */
+int mr_fp64_peak(mr_ctx* ctx, double* tflops);
+/* enable/disable CUDA-graph replay of the slow step (default on) */
+int mr_set_graphs(mr_ctx* ctx, int enable);
+/* record CUDA events around every launch class of a step (default off) */
+int mr_set_profiling(mr_ctx* ctx, int enable);
+/* per-kernel-class device time of the last step (ms), from CUDA events */
+int mr_last_step_profile(const mr_ctx* ctx, double* chem_ms, double* slow_ms, double* other_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,479 @@
+"""B200-native MRI slow step -- Python mirror of the reference stepper API.
+
+The product is ``libmri_b200.so`` (C-ABI in ``include/mri_b200.h``: host C++
+stage loop + hand-written sm_100a kernels).  This module is a thin ctypes
+binding that mirrors the reference's C++ interface for the hot path
+(/root/reference/proj/include/multirate/mri.hpp:64-133,
+partitioned_system.hpp:25-79, state_vector.hpp:22-36) so tests and the
+benchmark read like the reference's own code:
+
+    ctx = Context(device=0)
+    ctx.grid(n, n, n, ncomp)
+    ctx.method(coupling="mis-kw3", fast_table="classic-rk4", m=10)   # MriMethodConfig
+    ctx.fast_chemistry(...); ctx.slow_stencil(...)                  # PartitionedSystem
+    ctx.upload(y0)
+    ctx.mri_step(t, H, counters)        # raises ContractError / IntegrationError
+
+There is no CPU fallback: if the CUDA library is missing or no GPU is
+visible, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import tables
+from .configs import CONFIGS
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmri_b200.so")
+COUPLING_DIR = os.path.join(HERE, "data", "couplings")
+
+MR_OK, MR_CONTRACT, MR_INTEGRATION, MR_CUDA = 0, 1, 2, 3
+COUNTER_NAMES = ("n_fast_evals", "n_implicit_evals", "n_explicit_evals", "n_implicit_solves",
+                 "n_nonlinear_iters", "n_linear_iters", "n_precond_solves", "n_fast_ivps")
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_u64p = C.POINTER(C.c_uint64)
+
+
+class ContractError(ValueError):
+    """multirate::ContractError (state_vector.hpp:22-25)."""
+
+
+class IntegrationError(RuntimeError):
+    """multirate::IntegrationError with stage_index (state_vector.hpp:30-36)."""
+
+    def __init__(self, msg, stage_index=-1):
+        super().__init__(msg)
+        self.stage_index = stage_index
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def build(quiet: bool = True) -> None:
+    import subprocess
+    out = subprocess.DEVNULL if quiet else None
+    subprocess.run(["make", "-C", HERE, "-j8"], check=True, stdout=out)
+
+
+def lib():
+    """Load libmri_b200.so (fails loudly when it is missing -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run paper_2211_03293_b200.build() "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp = C.c_void_p
+    sig = {
+        "mr_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+        "mr_ctx_destroy": (None, [vp]),
+        "mr_last_error": (C.c_char_p, [vp]),
+        "mr_version": (C.c_int, []),
+        "mr_grid_set": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int]),
+        "mr_coupling_load": (C.c_int, [vp, C.c_int, C.c_int, _dp, _ip, _dp, _dp]),
+        "mr_coupling_load_text": (C.c_int, [vp, C.c_char_p]),
+        "mr_table_load": (C.c_int, [vp, C.c_int, _dp, _dp, _dp]),
+        "mr_set_substeps": (C.c_int, [vp, C.c_int]),
+        "mr_fast_chemistry": (C.c_int, [vp, C.c_int, C.c_int, C.c_double, _dp, _dp, _ip]),
+        "mr_fast_linear": (C.c_int, [vp, _dp]),
+        "mr_fast_none": (C.c_int, [vp]),
+        "mr_slow_stencil": (C.c_int, [vp, C.c_int, C.c_double, _dp, _dp, C.c_int]),
+        "mr_slow_linear": (C.c_int, [vp, _dp]),
+        "mr_slow_none": (C.c_int, [vp]),
+        "mr_state_upload": (C.c_int, [vp, _dp]),
+        "mr_state_download": (C.c_int, [vp, _dp]),
+        "mr_state_device_ptr": (C.c_void_p, [vp]),
+        "mr_state_dof": (C.c_size_t, [vp]),
+        "mr_mri_step": (C.c_int, [vp, C.c_double, C.c_double, _u64p, _ip]),
+        "mr_mri_integrate": (C.c_int, [vp, C.c_double, C.c_double, C.c_double, _u64p, _ip]),
+        "mr_mri_step_host": (C.c_int, [vp, C.c_double, C.c_double, _dp, _dp, _u64p, _ip]),
+        "mr_last_failure": (C.c_int, [vp, _ip, _ip, _ip]),
+        "mr_fast_rhs": (C.c_int, [vp, C.c_double, _dp, _dp]),
+        "mr_slow_rhs": (C.c_int, [vp, C.c_double, _dp, _dp]),
+        "mr_wrms_norm": (C.c_int, [vp, C.c_void_p, C.c_void_p, C.c_size_t, _dp]),
+        "mr_two_norm": (C.c_int, [vp, C.c_void_p, C.c_size_t, _dp]),
+        "mr_dot": (C.c_int, [vp, C.c_void_p, C.c_void_p, C.c_size_t, _dp]),
+        "mr_max_norm": (C.c_int, [vp, C.c_void_p, C.c_size_t, _dp]),
+        "mr_max_norm_component": (C.c_int, [vp, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, _dp]),
+        "mr_all_finite": (C.c_int, [vp, C.c_void_p, C.c_size_t, _ip]),
+        "mr_nccl_unique_id": (C.c_int, [C.c_char_p]),
+        "mr_comm_init": (C.c_int, [vp, C.c_int, C.c_int, C.c_char_p]),
+        "mr_group_step": (C.c_int, [C.POINTER(vp), C.c_int, C.c_double, C.c_double, _u64p, _ip]),
+        "mr_mechanism_generate": (C.c_int, [C.c_uint64, C.c_int, C.c_int, _dp, _dp, _ip]),
+        "mr_initial_condition": (C.c_int, [C.c_uint64, C.c_int, C.c_double, _dp, C.c_int, C.c_int,
+                                           C.c_int, C.c_double, C.c_int, C.c_int, _dp, C.c_int]),
+        "mr_velocity_profiles": (C.c_int, [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_double, _dp]),
+        "mr_coupling_inspect": (C.c_int, [C.c_char_p, C.c_int, _ip, _ip, _ip, _ip, C.c_char_p,
+                                          C.c_size_t]),
+        "mr_step_counts": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, _u64p,
+                                     C.c_char_p, C.c_size_t]),
+        "mr_stream": (C.c_void_p, [vp]),
+        "mr_launch_count": (C.c_uint64, [vp]),
+        "mr_chem_flops_per_eval": (C.c_double, [vp]),
+        "mr_fp64_peak": (C.c_int, [vp, _dp]),
+        "mr_set_graphs": (C.c_int, [vp, C.c_int]),
+        "mr_set_profiling": (C.c_int, [vp, C.c_int]),
+        "mr_last_step_profile": (C.c_int, [vp, _dp, _dp, _dp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _p(a, t=_dp):
+    return a.ctypes.data_as(t)
+
+
+# --------------------------------------------------------------------------
+# host-side generators (product implementation, C++)
+# --------------------------------------------------------------------------
+def mechanism(seed: int, S: int, R: int):
+    sp = np.zeros(5 * S)
+    rx = np.zeros(3 * R)
+    rs = np.zeros(4 * R, dtype=np.int32)
+    if lib().mr_mechanism_generate(seed, S, R, _p(sp), _p(rx), _p(rs, _ip)):
+        raise ContractError("mr_mechanism_generate: bad arguments")
+    return sp, rx, rs
+
+
+def velocity_profiles(seed: int, n0: int, n1: int, n2: int, length: float = 1.0):
+    prof = np.zeros(6 * max(n0, n1, n2))
+    lib().mr_velocity_profiles(seed, n0, n1, n2, length, _p(prof))
+    return prof
+
+
+def initial_condition(seed, S, rho, species, n0, n1, n2, length=1.0, i0=0, n0_local=None,
+                      threads=0, out=None):
+    n0l = n0 if n0_local is None else n0_local
+    dof = (S + 1) * n0l * n1 * n2
+    Y = np.empty(dof) if out is None else out
+    sp = np.ascontiguousarray(species, dtype=np.float64)
+    rc = lib().mr_initial_condition(seed, S, rho, _p(sp), n0, n1, n2, length, i0, n0l, _p(Y),
+                                    threads)
+    if rc:
+        raise ContractError("mr_initial_condition: bad arguments")
+    return Y
+
+
+def coupling_text(name: str) -> str:
+    """v1 audit text of a coupling (the reference's export_coupling output,
+    shipped in data/couplings/)."""
+    if name.startswith("mri-coupling"):
+        return name
+    path = os.path.join(COUPLING_DIR, f"{name}.txt")
+    if not os.path.exists(path):
+        raise ContractError(f"register_coupling: unknown name '{name}'")
+    with open(path) as f:
+        return f.read()
+
+
+def coupling_inspect(coupling: str, m: int = 1):
+    """Host-side parse + finalize (reference rules, mri.cpp:59-167); raises
+    ContractError with the reference's message on a structural violation."""
+    s = C.c_int()
+    kinds = np.zeros(16, dtype=np.int32)
+    ev = np.zeros(16, dtype=np.int32)
+    ns = np.zeros(16, dtype=np.int32)
+    err = C.create_string_buffer(512)
+    rc = lib().mr_coupling_inspect(coupling_text(coupling).encode(), m, C.byref(s), _p(kinds, _ip),
+                                   _p(ev, _ip), _p(ns, _ip), err, 512)
+    if rc:
+        raise ContractError(err.value.decode())
+    n = s.value
+    return dict(s=n, kinds=kinds[:n].tolist(), eval_at=ev[:n].tolist(), n_sub=ns[:n].tolist())
+
+
+def step_counts(coupling: str, fast_table: str, m: int, fast=True, slow=True):
+    """EvalCounters increments of one slow step as planned by the device loop."""
+    cnt = np.zeros(8, dtype=np.uint64)
+    err = C.create_string_buffer(512)
+    s_f = len(tables.lookup_table(fast_table)["b"])
+    rc = lib().mr_step_counts(coupling_text(coupling).encode(), s_f, m, int(fast), int(slow),
+                              _p(cnt, _u64p), err, 512)
+    if rc == MR_CONTRACT:
+        raise ContractError(err.value.decode())
+    if rc:
+        raise IntegrationError(err.value.decode())
+    return cnt
+
+
+# --------------------------------------------------------------------------
+class Context:
+    """One device-resident MRI problem (one slab of the grid)."""
+
+    def __init__(self, device: int = 0):
+        L = lib()
+        h = C.c_void_p()
+        rc = L.mr_ctx_create(device, C.byref(h))
+        if rc:
+            raise CudaError(f"mr_ctx_create failed (rc={rc}): no usable B200 / CUDA device")
+        self.h = h
+        self.L = L
+        self.dof = 0
+        self.s_f = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.mr_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc, stage=None):
+        if rc == MR_OK:
+            return
+        msg = self.L.mr_last_error(self.h).decode()
+        if rc == MR_CONTRACT:
+            raise ContractError(msg)
+        if rc == MR_INTEGRATION:
+            raise IntegrationError(msg, -1 if stage is None else stage)
+        raise CudaError(msg)
+
+    # ---- setup -------------------------------------------------------------
+    def grid(self, n0, n1, n2, ncomp, length=1.0, i0=0, n0_local=None):
+        n0l = n0 if n0_local is None else n0_local
+        self._check(self.L.mr_grid_set(self.h, n0, n1, n2, ncomp, length, i0, n0l))
+        self.shape = (n0, n1, n2)
+        self.ncomp = ncomp
+        self.ncell = n0l * n1 * n2
+        self.dof = self.ncell * ncomp
+        return self
+
+    def method(self, coupling="mis-kw3", fast_table="classic-rk4", m=1):
+        """MriMethodConfig (mri.hpp:64-68)."""
+        self.load_coupling(coupling)
+        self.load_table(fast_table)
+        self._check(self.L.mr_set_substeps(self.h, m))
+        return self
+
+    def load_coupling(self, coupling):
+        self._check(self.L.mr_coupling_load_text(self.h, coupling_text(coupling).encode()))
+
+    def load_coupling_arrays(self, c, kind, gamma, omega):
+        s = len(c)
+        cc = np.ascontiguousarray(c, dtype=np.float64)
+        kk = np.ascontiguousarray(kind, dtype=np.int32)
+        g = None if gamma is None else np.ascontiguousarray(gamma, dtype=np.float64)
+        o = None if omega is None else np.ascontiguousarray(omega, dtype=np.float64)
+        nd = (g if g is not None else o).size // (s * s)
+        self._check(self.L.mr_coupling_load(self.h, s, nd, _p(cc), _p(kk, _ip),
+                                            None if g is None else _p(g),
+                                            None if o is None else _p(o)))
+
+    def load_table(self, name_or_table):
+        t = tables.lookup_table(name_or_table) if isinstance(name_or_table, str) else name_or_table
+        A = np.ascontiguousarray(t["A"], dtype=np.float64)
+        b = np.ascontiguousarray(t["b"], dtype=np.float64)
+        c = np.ascontiguousarray(t["c"], dtype=np.float64)
+        self._check(self.L.mr_table_load(self.h, len(b), _p(A), _p(b), _p(c)))
+        self.s_f = len(b)
+
+    def fast_chemistry(self, S, R, rho, species, reactions, rspecies):
+        sp = np.ascontiguousarray(species, dtype=np.float64)
+        rx = np.ascontiguousarray(reactions, dtype=np.float64)
+        rs = np.ascontiguousarray(rspecies, dtype=np.int32)
+        self._check(self.L.mr_fast_chemistry(self.h, S, R, rho, _p(sp), _p(rx), _p(rs, _ip)))
+
+    def fast_linear(self, A):
+        a = np.ascontiguousarray(A, dtype=np.float64).ravel()
+        self._check(self.L.mr_fast_linear(self.h, _p(a)))
+
+    def fast_none(self):
+        self._check(self.L.mr_fast_none(self.h))
+
+    def slow_stencil(self, order, diffusion, u=(1.0, 1.0, 1.0), prof=None):
+        if prof is not None:
+            pr = np.ascontiguousarray(prof, dtype=np.float64)
+            self._check(self.L.mr_slow_stencil(self.h, order, diffusion, None, _p(pr), pr.size // 6))
+        else:
+            uu = np.ascontiguousarray(u, dtype=np.float64)
+            self._check(self.L.mr_slow_stencil(self.h, order, diffusion, _p(uu), None, 0))
+
+    def slow_linear(self, A):
+        a = np.ascontiguousarray(A, dtype=np.float64).ravel()
+        self._check(self.L.mr_slow_linear(self.h, _p(a)))
+
+    def slow_none(self):
+        self._check(self.L.mr_slow_none(self.h))
+
+    # ---- state ---------------------------------------------------------------
+    def upload(self, y):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        assert y.size == self.dof, (y.size, self.dof)
+        self._check(self.L.mr_state_upload(self.h, _p(y)))
+
+    def download(self, out=None):
+        y = np.empty(self.dof) if out is None else out
+        self._check(self.L.mr_state_download(self.h, _p(y)))
+        return y
+
+    def state_ptr(self):
+        return self.L.mr_state_device_ptr(self.h)
+
+    # ---- stepping ---------------------------------------------------------------
+    @staticmethod
+    def counters():
+        return np.zeros(8, dtype=np.uint64)
+
+    def mri_step(self, t, H, counters=None):
+        cnt = self.counters() if counters is None else counters
+        stage = C.c_int(-1)
+        rc = self.L.mr_mri_step(self.h, t, H, _p(cnt, _u64p), C.byref(stage))
+        self._check(rc, stage.value)
+        return cnt
+
+    def mri_integrate(self, t0, tf, H, counters=None):
+        cnt = self.counters() if counters is None else counters
+        stage = C.c_int(-1)
+        rc = self.L.mr_mri_integrate(self.h, t0, tf, H, _p(cnt, _u64p), C.byref(stage))
+        self._check(rc, stage.value)
+        return cnt
+
+    def mri_step_host(self, t, H, y_in, y_out, counters=None):
+        cnt = self.counters() if counters is None else counters
+        stage = C.c_int(-1)
+        rc = self.L.mr_mri_step_host(self.h, t, H, _p(y_in), _p(y_out), _p(cnt, _u64p),
+                                     C.byref(stage))
+        self._check(rc, stage.value)
+        return cnt
+
+    def last_failure(self):
+        a, b, c = C.c_int(), C.c_int(), C.c_int()
+        self.L.mr_last_failure(self.h, C.byref(a), C.byref(b), C.byref(c))
+        return a.value, b.value, c.value
+
+    def fast_rhs(self, y, t=0.0):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        out = np.empty_like(y)
+        self._check(self.L.mr_fast_rhs(self.h, t, _p(y), _p(out)))
+        return out
+
+    def slow_rhs(self, y, t=0.0):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        out = np.empty_like(y)
+        self._check(self.L.mr_slow_rhs(self.h, t, _p(y), _p(out)))
+        return out
+
+    # ---- reductions over device pointers (state by default) ---------------
+    def _red(self, fn, *args):
+        out = C.c_double()
+        self._check(fn(self.h, *args, C.byref(out)))
+        return out.value
+
+    def wrms_norm(self, x_ptr, w_ptr, n):
+        return self._red(self.L.mr_wrms_norm, x_ptr, w_ptr, n)
+
+    def two_norm(self, x_ptr, n):
+        return self._red(self.L.mr_two_norm, x_ptr, n)
+
+    def dot(self, x_ptr, y_ptr, n):
+        return self._red(self.L.mr_dot, x_ptr, y_ptr, n)
+
+    def max_norm(self, x_ptr, n):
+        return self._red(self.L.mr_max_norm, x_ptr, n)
+
+    def max_norm_component(self, x_ptr, n, offset, count):
+        return self._red(self.L.mr_max_norm_component, x_ptr, n, offset, count)
+
+    def all_finite(self, x_ptr, n):
+        out = C.c_int()
+        self._check(self.L.mr_all_finite(self.h, x_ptr, n, C.byref(out)))
+        return bool(out.value)
+
+    # ---- instrumentation ---------------------------------------------------
+    def stream(self):
+        return self.L.mr_stream(self.h)
+
+    def launch_count(self):
+        return int(self.L.mr_launch_count(self.h))
+
+    def chem_flops_per_eval(self):
+        return float(self.L.mr_chem_flops_per_eval(self.h))
+
+    def fp64_peak(self):
+        out = C.c_double()
+        self._check(self.L.mr_fp64_peak(self.h, C.byref(out)))
+        return out.value
+
+    def set_profiling(self, on=True):
+        self._check(self.L.mr_set_profiling(self.h, int(on)))
+
+    def last_step_profile(self):
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        self._check(self.L.mr_last_step_profile(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    # ---- multi-GPU -----------------------------------------------------------
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        if lib().mr_nccl_unique_id(buf):
+            raise CudaError("ncclGetUniqueId failed")
+        return buf.raw
+
+    def comm_init(self, nranks, rank, uid: bytes):
+        self._check(self.L.mr_comm_init(self.h, nranks, rank, uid))
+
+
+def group_step(ctxs, t, H, counters=None):
+    """One slow step of several slab contexts on one device ("virtual ranks")."""
+    L = lib()
+    arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+    cnt = Context.counters() if counters is None else counters
+    stage = C.c_int(-1)
+    rc = L.mr_group_step(arr, len(ctxs), t, H, _p(cnt, _u64p), C.byref(stage))
+    ctxs[0]._check(rc, stage.value)
+    return cnt
+
+
+def slab_bounds(n0: int, nranks: int, rank: int):
+    """Slab decomposition along axis 0: equal slabs, remainder to the first ranks."""
+    base, rem = divmod(n0, nranks)
+    n0l = base + (1 if rank < rem else 0)
+    i0 = rank * base + min(rank, rem)
+    return i0, n0l
+
+
+def setup_workload(ctx: Context, name: str, *, n=None, i0=0, n0_local=None, threads=0,
+                   make_state=True, config=None):
+    """Configure ctx for a BASELINE.json workload (C1-C4), optionally on a
+    smaller grid n and a slab [i0, i0+n0_local); returns (cfg, y0)."""
+    cfg = dict(CONFIGS[name] if config is None else config)
+    if n is not None:
+        cfg["n"] = n
+    N = cfg["n"]
+    S, R = cfg["S"], cfg["R"]
+    n0l = N if n0_local is None else n0_local
+    ctx.grid(N, N, N, S + 1, 1.0, i0, n0l)
+    ctx.method(cfg["coupling"], cfg["fast_table"], cfg["m"])
+    sp, rx, rs = mechanism(cfg["mech_seed"], S, R)
+    ctx.fast_chemistry(S, R, cfg["rho"], sp, rx, rs)
+    if cfg["velocity"] == "uniform":
+        ctx.slow_stencil(cfg["order"], cfg["diffusion"], u=cfg["u"])
+    else:
+        ctx.slow_stencil(cfg["order"], cfg["diffusion"],
+                         prof=velocity_profiles(cfg["vel_seed"], N, N, N))
+    y0 = None
+    if make_state:
+        y0 = initial_condition(cfg["ic_seed"], S, cfg["rho"], sp, N, N, N, 1.0, i0, n0l, threads)
+        ctx.upload(y0)
+    cfg["mech"] = (sp, rx, rs)
+    return cfg, y0

@@ -1,0 +1,132 @@
+// common.cuh -- shared device-side structures of libmri_b200.so.
+//
+// Layout in HBM: every state-sized vector is
+// species-major, Y[comp * ncell + cell], cell = (i * n1 + j) * n2 + k over the
+// local slab (axis 0 sharded), exactly the reference's host layout
+// (proj/src/models.cpp:117-125, :155-157) so uploads are a single memcpy.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#define MR_MAXS 6      // inner ERK stages (butcher tables up to cash-karp5)
+#define MR_MAXDEG 2    // forcing-polynomial coefficients (gark4 uses 2)
+#define MR_MAXREF 8    // referenced slow-RHS stage values per MRI stage
+#define MR_MAXCHAIN 6  // cell-local MRI stages fused into one launch
+#define MR_MAXSLOT 16  // stored slow-RHS stage values
+#define MR_MAXLIN 8    // components of the linear test plugins
+
+// Explicit Butcher table (butcher.hpp:16-27)
+struct TableDev {
+  int s;
+  double A[MR_MAXS][MR_MAXS];
+  double b[MR_MAXS];
+  double c[MR_MAXS];
+};
+
+// One cell-local MRI stage inside a fused chain (mri.cpp:354-426):
+//  kind 0 = FastIvp: build_forcing + n_sub inner ERK steps
+//  kind 2 = ExplicitUpdate: Y += sum_j (H wbar_ij) fE_j
+struct ChainStageDev {
+  int kind;
+  int mri_stage;
+  int n_sub;
+  int nref;
+  double t_start, span, h_sub;
+  int ref_slot[MR_MAXREF];
+  // FastIvp: coef[k][r] = omega[k][i][j_r] / dc (0 => term skipped, as
+  // build_forcing's `if (coef == 0.0) continue`); Update: coef[0][r] = H*wbar
+  double coef[MR_MAXDEG][MR_MAXREF];
+};
+
+struct ChainArgs {
+  int nst;
+  int ndeg;  // r.coeffs.size() = max(degrees, 1)
+  ChainStageDev st[MR_MAXCHAIN];
+  TableDev tab;
+  const double* y_in;
+  double* y_out;
+  const double* fE[MR_MAXSLOT];
+  size_t ncell;
+  int ncomp;
+  unsigned long long* fail;
+};
+
+// Per-cell synthetic Arrhenius chemistry
+struct ChemDev {
+  int S, R, Spad;
+  const double4* rxn;    // {lnA, beta, Ea/Rc, dnu}
+  const int4* rsp;       // {r1, r2, p1, p2}, absent -> S (dummy slot = 1)
+  const double* sp;      // SoA [9][Spad]: h0, a, hb, s0, rhoW, Wrho, c0, c1, c2
+  const int* csr_off;    // [S+1]
+  const int* csr_ent;    // reaction*2 + (product ? 1 : 0), reaction ascending
+  double RuP;            // R_u / P_atm
+};
+
+struct LinDev {
+  int n;
+  double A[MR_MAXLIN * MR_MAXLIN];
+};
+
+// Slow RHS (stencil) arguments
+struct StencilArgs {
+  const double* y;
+  double* out;
+  const double* halo_lo;  // [comp][g][n1*n2]: planes i0-g .. i0-1
+  const double* halo_hi;  // [comp][g][n1*n2]: planes i0+n0l .. i0+n0l+g-1
+  int n0l, n1, n2, ncomp, M;
+  int i0;                 // global index of the first local plane
+  double a[5], b[5];
+  double inv_dx[3], inv_dx2[3];
+  double D;
+  int vel_kind;
+  double u[3];
+  const double* prof;     // [3][2][nmax]
+  int nmax;
+};
+
+enum FastKind { FK_NONE = 0, FK_CHEM = 1, FK_LINEAR = 2 };
+enum SlowKind { SK_NONE = 0, SK_STENCIL = 1, SK_LINEAR = 2 };
+
+// failure key, ordered like the reference's execution order
+__host__ __device__ inline unsigned long long mr_fail_key(int mri_stage, int sub, int inner)
+{
+  return ((unsigned long long)mri_stage << 40) | ((unsigned long long)sub << 8) |
+         (unsigned long long)inner;
+}
+#define MR_NO_FAIL 0xFFFFFFFFFFFFFFFFull
+
+// ---------------- launchers (defined in the .cu files) ----------------
+#include <cuda_runtime.h>
+
+// chain kernel configuration chosen by the host
+struct ChainCfg {
+  int fast_kind;
+  int G;     // lanes per cell
+  int SPL;   // components per lane
+  int maxs;  // 4 or 6
+  int ndeg;  // 1 or 2
+};
+int chain_pick(ChainCfg* cfg, int fast_kind, int ncomp, int S, int R, int s_f, int ndeg);
+cudaError_t launch_chain(const ChainCfg& cfg, const ChainArgs& a, const ChemDev& ch,
+                         const LinDev& lin, cudaStream_t st);
+cudaError_t launch_fast_rhs(const ChainCfg& cfg, const double* y, double* out, size_t ncell,
+                            int ncomp, const ChemDev& ch, const LinDev& lin, cudaStream_t st);
+size_t chain_smem_bytes(const ChainCfg& cfg, int S, int R, int block);
+
+cudaError_t launch_update(const double* y_in, double* y_out, int nref, const double* const* f,
+                          const double* coef, size_t n, int mri_stage,
+                          unsigned long long* fail, cudaStream_t st);
+cudaError_t launch_stencil(const StencilArgs& a, cudaStream_t st);
+cudaError_t launch_slow_linear(const double* y, double* out, size_t ncell, const LinDev& lin,
+                               cudaStream_t st);
+cudaError_t launch_halo_pack(const double* y, double* send_lo, double* send_hi, int ncomp,
+                             int n0l, size_t plane, int g, cudaStream_t st);
+
+// reductions: result written to *d_out (device); fixed-order two-pass
+enum RedKind { RED_WRMS = 0, RED_TWO = 1, RED_DOT = 2, RED_MAX = 3, RED_NONFINITE = 4 };
+cudaError_t launch_reduce(int kind, const double* x, const double* w, size_t n, double* d_part,
+                          int nblocks, double* d_out, cudaStream_t st);
+int reduce_blocks();
+
+cudaError_t launch_fp64_peak(double* sink, int blocks, int threads, int iters, cudaStream_t st);

@@ -1,0 +1,313 @@
+// kernels_slow.cu -- K2 slow RHS (3D periodic centred advection-diffusion),
+// K3 stand-alone explicit update, halo packing, the per-cell linear slow
+// plugin, K4 reductions and the fp64 peak microbenchmark.
+//
+// K2 replaces rhs_advection + rhs_diffusion (proj/src/models.cpp:129-211)
+// summed by slow_rhs (proj/include/multirate/partitioned_system.hpp:54-60),
+// extended to 3D and orders 2/4/8.  Formula and term order follow the oracle
+// (oracle/mri_oracle.c sten_range); HBM-bound: 8*ncomp*ncell bytes read and
+// written once per evaluation.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace {
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+// Axis-0 neighbours come from the local slab or from the halo planes
+// (exchanged over NCCL / copied for the periodic single-slab case); axes 1
+// and 2 wrap periodically inside the slab.  One thread per cell, looping over
+// components so the per-cell velocity coefficients are computed once.
+__global__ void __launch_bounds__(256) stencil_kernel(const StencilArgs a)
+{
+  const size_t plane = (size_t)a.n1 * a.n2;
+  const size_t ncell = plane * (size_t)a.n0l;
+  const size_t cell = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= ncell) return;
+  const int i = (int)(cell / plane);
+  const size_t rem = cell - (size_t)i * plane;
+  const int j = (int)(rem / a.n2);
+  const int k = (int)(rem - (size_t)j * a.n2);
+  const int M = a.M;
+
+  double u[3];
+  if (a.vel_kind == 0) {
+    u[0] = a.u[0]; u[1] = a.u[1]; u[2] = a.u[2];
+  } else {
+    const int ig = a.i0 + i;
+    const double* P = a.prof;
+    const int nm = a.nmax;
+    u[0] = P[(0 * 2 + 0) * nm + j] + P[(0 * 2 + 1) * nm + k];
+    u[1] = P[(1 * 2 + 0) * nm + ig] + P[(1 * 2 + 1) * nm + k];
+    u[2] = P[(2 * 2 + 0) * nm + ig] + P[(2 * 2 + 1) * nm + j];
+  }
+  double cdif[3], cadv[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    cdif[d] = a.D * a.inv_dx2[d];
+    cadv[d] = u[d] * a.inv_dx[d];
+  }
+  // neighbour addressing, computed once per cell
+  int sel0[9];            // axis 0: 0 = slab, 1 = halo_lo, 2 = halo_hi
+  size_t off0[9];
+  long off1[9], off2[9];  // axes 1, 2 (relative, wrapped)
+#pragma unroll
+  for (int m = -4; m <= 4; ++m) {
+    const int q = m + 4;
+    const int ip = i + m;
+    if (ip < 0) { sel0[q] = 1; off0[q] = (size_t)(ip + M) * plane + rem; }
+    else if (ip >= a.n0l) { sel0[q] = 2; off0[q] = (size_t)(ip - a.n0l) * plane + rem; }
+    else { sel0[q] = 0; off0[q] = (size_t)ip * plane + rem; }
+    const int jp = ((j + m) % a.n1 + a.n1) % a.n1;
+    const int kp = ((k + m) % a.n2 + a.n2) % a.n2;
+    off1[q] = (long)(jp - j) * a.n2;
+    off2[q] = (long)(kp - k);
+  }
+  const size_t hstride = (size_t)M * plane;
+  for (int comp = 0; comp < a.ncomp; ++comp) {
+    const double* __restrict__ y = a.y + (size_t)comp * ncell;
+    const double* lo = a.halo_lo + (size_t)comp * hstride;
+    const double* hi = a.halo_hi + (size_t)comp * hstride;
+    const double yc = y[cell];
+    double acc = 0.0;
+    // axis 0
+    {
+      double adv = 0.0, dif = a.b[0] * yc;
+      for (int m = 1; m <= M; ++m) {
+        const int qp = 4 + m, qm = 4 - m;
+        const double* bp = sel0[qp] == 0 ? y : (sel0[qp] == 1 ? lo : hi);
+        const double* bm = sel0[qm] == 0 ? y : (sel0[qm] == 1 ? lo : hi);
+        const double yp = bp[off0[qp]], ym = bm[off0[qm]];
+        adv += a.a[m] * (yp - ym);
+        dif += a.b[m] * (yp + ym);
+      }
+      acc += cdif[0] * dif - cadv[0] * adv;
+    }
+    // axis 1
+    {
+      double adv = 0.0, dif = a.b[0] * yc;
+      for (int m = 1; m <= M; ++m) {
+        const double yp = y[cell + off1[4 + m]], ym = y[cell + off1[4 - m]];
+        adv += a.a[m] * (yp - ym);
+        dif += a.b[m] * (yp + ym);
+      }
+      acc += cdif[1] * dif - cadv[1] * adv;
+    }
+    // axis 2
+    {
+      double adv = 0.0, dif = a.b[0] * yc;
+      for (int m = 1; m <= M; ++m) {
+        const double yp = y[cell + off2[4 + m]], ym = y[cell + off2[4 - m]];
+        adv += a.a[m] * (yp - ym);
+        dif += a.b[m] * (yp + ym);
+      }
+      acc += cdif[2] * dif - cadv[2] * adv;
+    }
+    a.out[(size_t)comp * ncell + cell] = acc;
+  }
+}
+
+// halo planes: send_lo = first g planes, send_hi = last g planes, per component
+__global__ void halo_pack_kernel(const double* __restrict__ y, double* __restrict__ send_lo,
+                                 double* __restrict__ send_hi, int ncomp, int n0l, size_t plane,
+                                 int g)
+{
+  const size_t per = (size_t)g * plane;
+  const size_t total = per * ncomp;
+  const size_t ncell = plane * n0l;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t comp = idx / per, r = idx - comp * per;
+    send_lo[idx] = y[comp * ncell + r];
+    send_hi[idx] = y[comp * ncell + (size_t)(n0l - g) * plane + r];
+  }
+}
+
+// stand-alone ExplicitUpdate (mri.cpp:380-384, :422-424) + all_finite
+// (mri.cpp:427-431) for update-only chains
+struct UpdArgs {
+  const double* y_in;
+  double* y_out;
+  int nref;
+  const double* f[MR_MAXREF];
+  double coef[MR_MAXREF];
+  size_t n;
+  int mri_stage;
+  unsigned long long* fail;
+};
+
+__global__ void __launch_bounds__(256) update_kernel(const UpdArgs a)
+{
+  bool bad = false;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < a.n;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    double y = a.y_in[idx];
+    for (int r = 0; r < a.nref; ++r)
+      if (a.coef[r] != 0.0) y = dadd(y, dmul(a.coef[r], a.f[r][idx]));
+    a.y_out[idx] = y;
+    bad |= !isfinite(y);
+  }
+  if (bad) atomicMin(a.fail, mr_fail_key(a.mri_stage, 0, 0));
+}
+
+__global__ void __launch_bounds__(256) slow_linear_kernel(const double* __restrict__ y,
+                                                          double* __restrict__ out, size_t nc,
+                                                          const LinDev L)
+{
+  const size_t cell = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= nc) return;
+  double v[MR_MAXLIN];
+#pragma unroll
+  for (int b = 0; b < MR_MAXLIN; ++b) v[b] = b < L.n ? y[(size_t)b * nc + cell] : 0.0;
+  for (int a2 = 0; a2 < L.n; ++a2) {
+    double acc = dmul(L.A[a2 * L.n], v[0]);
+#pragma unroll
+    for (int b = 1; b < MR_MAXLIN; ++b)
+      if (b < L.n) acc = dadd(acc, dmul(L.A[a2 * L.n + b], v[b]));
+    out[(size_t)a2 * nc + cell] = acc;
+  }
+}
+
+// ---------------- K4 reductions (fixed-order two-pass) ----------------
+constexpr int kRedThreads = 256;
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs; fixed so results are run-to-run bitwise
+
+__device__ __forceinline__ double red_op(int kind, double a, double b)
+{
+  if (kind == RED_MAX) return (a < b) ? b : a;  // std::max semantics: NaN ignored
+  return a + b;
+}
+
+__global__ void __launch_bounds__(kRedThreads) reduce_partial(int kind, const double* __restrict__ x,
+                                                             const double* __restrict__ w, size_t n,
+                                                             double* __restrict__ part)
+{
+  double acc = 0.0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const double v = x[i];
+    double t;
+    switch (kind) {
+      case RED_WRMS: { const double xw = v * w[i]; t = xw * xw; break; }
+      case RED_TWO: t = v * v; break;
+      case RED_DOT: t = v * w[i]; break;
+      case RED_MAX: t = fabs(v); break;
+      default: t = isfinite(v) ? 0.0 : 1.0; break;
+    }
+    acc = red_op(kind == RED_NONFINITE ? RED_TWO : kind, acc, t);
+  }
+  __shared__ double sh[kRedThreads];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = kRedThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+      sh[threadIdx.x] = red_op(kind == RED_NONFINITE ? RED_TWO : kind, sh[threadIdx.x],
+                               sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(1024) reduce_final(int kind, const double* __restrict__ part,
+                                                    int np, size_t n, double* __restrict__ out)
+{
+  __shared__ double sh[1024];
+  const int op = kind == RED_NONFINITE ? RED_TWO : kind;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc = red_op(op, acc, part[i]);
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] = red_op(op, sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double r = sh[0];
+    if (kind == RED_WRMS) r = sqrt(r / (double)n);
+    else if (kind == RED_TWO) r = sqrt(r);
+    out[0] = r;
+  }
+}
+
+__global__ void fp64_peak_kernel(double* sink, int iters)
+{
+  double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-3, x2 = x0 + 2e-3, x3 = x0 + 3e-3;
+  double x4 = x0 + 4e-3, x5 = x0 + 5e-3, x6 = x0 + 6e-3, x7 = x0 + 7e-3;
+  const double a = 0.999999, b = 1e-7;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 12345.678) sink[0] = s;  // keep the chains alive
+}
+
+}  // namespace
+
+cudaError_t launch_stencil(const StencilArgs& a, cudaStream_t st)
+{
+  const size_t ncell = (size_t)a.n0l * a.n1 * a.n2;
+  stencil_kernel<<<(unsigned)((ncell + 255) / 256), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_halo_pack(const double* y, double* send_lo, double* send_hi, int ncomp,
+                             int n0l, size_t plane, int g, cudaStream_t st)
+{
+  const size_t total = (size_t)g * plane * ncomp;
+  size_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks == 0) blocks = 1;
+  halo_pack_kernel<<<(unsigned)blocks, 256, 0, st>>>(y, send_lo, send_hi, ncomp, n0l, plane, g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update(const double* y_in, double* y_out, int nref, const double* const* f,
+                          const double* coef, size_t n, int mri_stage,
+                          unsigned long long* fail, cudaStream_t st)
+{
+  UpdArgs a;
+  a.y_in = y_in;
+  a.y_out = y_out;
+  a.nref = nref;
+  for (int r = 0; r < MR_MAXREF; ++r) {
+    a.f[r] = r < nref ? f[r] : nullptr;
+    a.coef[r] = r < nref ? coef[r] : 0.0;
+  }
+  a.n = n;
+  a.mri_stage = mri_stage;
+  a.fail = fail;
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks == 0) blocks = 1;
+  update_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_slow_linear(const double* y, double* out, size_t ncell, const LinDev& lin,
+                               cudaStream_t st)
+{
+  slow_linear_kernel<<<(unsigned)((ncell + 255) / 256), 256, 0, st>>>(y, out, ncell, lin);
+  return cudaGetLastError();
+}
+
+int reduce_blocks() { return kRedBlocks; }
+
+cudaError_t launch_reduce(int kind, const double* x, const double* w, size_t n, double* d_part,
+                          int nblocks, double* d_out, cudaStream_t st)
+{
+  reduce_partial<<<nblocks, kRedThreads, 0, st>>>(kind, x, w, n, d_part);
+  reduce_final<<<1, 1024, 0, st>>>(kind, d_part, nblocks, n, d_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fp64_peak(double* sink, int blocks, int threads, int iters, cudaStream_t st)
+{
+  fp64_peak_kernel<<<blocks, threads, 0, st>>>(sink, iters);
+  return cudaGetLastError();
+}

@@ -1,0 +1,1459 @@
+// mri_b200.cu -- host side of libmri_b200.so: context, method data, the MRI
+// slow-step stage loop and the C-ABI (include/mri_b200.h).
+//
+// The stage loop mirrors multirate::mri_step (proj/src/mri.cpp:323-435) for
+// fully explicit couplings, but instead of one full-vector pass per vector op
+// it compiles the coupling into a short plan of fused device launches:
+//
+//   SLOW(j)   K2 stencil: fE_j = f_slow(Y_j)        (eval_slow_at, mri.cpp:339-349)
+//   CHAIN     K1: maximal run of cell-local stages between two slow evaluations
+//             (fast IVPs with their forcing, explicit updates, finite checks)
+//   UPDATE    K3: explicit update when a run holds no fast IVP
+//
+// Counters follow the reference's increment rules exactly (mri.cpp:342, :347,
+// :378; erk.cpp:28), including partial counts on an IntegrationError.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/mri_b200.h"
+#include "common.cuh"
+
+namespace {
+
+constexpr double kRu = 8.31446261815324e7;  // erg/(mol K)
+constexpr double kPatm = 1.01325e6;         // dyn/cm^2
+constexpr double kConsistencyTol = 1.0e-12; // mri.cpp:14
+constexpr int kMaxStages = 16;
+
+struct Coupling {
+  std::string name;
+  int s = 0;
+  int ndeg_g = 0, ndeg_o = 0;
+  double c[kMaxStages] = {};
+  int kind[kMaxStages] = {};
+  std::vector<double> gamma, omega;  // [deg][s][s]
+  double gbar[kMaxStages][kMaxStages] = {};
+  double wbar[kMaxStages][kMaxStages] = {};
+  bool eval_at[kMaxStages] = {};
+  bool fE_ref[kMaxStages] = {};
+  bool fI_ref[kMaxStages] = {};
+  bool implicit = false;
+  double G(int k, int i, int j) const { return gamma[((size_t)k * s + i) * s + j]; }
+  double W(int k, int i, int j) const { return omega[((size_t)k * s + i) * s + j]; }
+  int degrees() const { return std::max(ndeg_g, ndeg_o); }
+};
+
+// MriCoupling::finalize (proj/src/mri.cpp:59-167): validation + derived data
+bool finalize(Coupling& cp, std::string& err)
+{
+  const int s = cp.s;
+  auto bad = [&](const std::string& m) {
+    err = "MriCoupling " + cp.name + ": " + m;
+    return false;
+  };
+  if (s < 2 || s > kMaxStages) return bad("inconsistent sizes");
+  if (std::fabs(cp.c[0]) > 0.0 || std::fabs(cp.c[s - 1] - 1.0) > kConsistencyTol)
+    return bad("need c[0]=0 and c[s-1]=1");
+  for (int i = 1; i < s; ++i)
+    if (cp.c[i] < cp.c[i - 1] - kConsistencyTol) return bad("abscissae decrease");
+  for (int pass = 0; pass < 2; ++pass) {
+    const int nd = pass == 0 ? cp.ndeg_g : cp.ndeg_o;
+    for (int k = 0; k < nd; ++k)
+      for (int i = 0; i < s; ++i)
+        for (int j = i; j < s; ++j) {
+          const double v = pass == 0 ? cp.G(k, i, j) : cp.W(k, i, j);
+          const bool diag_ok = pass == 0 && j == i && cp.kind[i] == MR_STAGE_IMPLICIT_SOLVE;
+          if (v != 0.0 && !diag_ok)
+            return bad(std::string(pass == 0 ? "gamma" : "omega") +
+                       " not lower triangular at stage " + std::to_string(i));
+        }
+  }
+  std::memset(cp.gbar, 0, sizeof(cp.gbar));
+  std::memset(cp.wbar, 0, sizeof(cp.wbar));
+  for (int k = 0; k < cp.ndeg_g; ++k) {
+    const double w = 1.0 / static_cast<double>(k + 1);
+    for (int i = 0; i < s; ++i)
+      for (int j = 0; j < s; ++j) cp.gbar[i][j] += w * cp.G(k, i, j);
+  }
+  for (int k = 0; k < cp.ndeg_o; ++k) {
+    const double w = 1.0 / static_cast<double>(k + 1);
+    for (int i = 0; i < s; ++i)
+      for (int j = 0; j < s; ++j) cp.wbar[i][j] += w * cp.W(k, i, j);
+  }
+  bool has_g = false, has_o = false;
+  for (double v : cp.gamma) has_g |= v != 0.0;
+  for (double v : cp.omega) has_o |= v != 0.0;
+  cp.implicit = has_g;
+  for (int i = 1; i < s; ++i) {
+    const double dc = cp.c[i] - cp.c[i - 1];
+    if (cp.kind[i] == MR_STAGE_FAST_IVP) {
+      if (dc <= 0.0) return bad("fast-ivp stage " + std::to_string(i) + " has dc <= 0");
+    } else {
+      if (dc > kConsistencyTol)
+        return bad("stage " + std::to_string(i) + " solves/updates with dc > 0");
+      if (cp.kind[i] == MR_STAGE_IMPLICIT_SOLVE && cp.gbar[i][i] == 0.0)
+        return bad("implicit stage " + std::to_string(i) + " has zero diagonal");
+    }
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool used = pass == 0 ? has_g : has_o;
+      if (!used) continue;
+      const int nd = pass == 0 ? cp.ndeg_g : cp.ndeg_o;
+      double bar_sum = 0.0;
+      for (int k = 0; k < nd; ++k) {
+        double rk = 0.0;
+        for (int j = 0; j < s; ++j) rk += pass == 0 ? cp.G(k, i, j) : cp.W(k, i, j);
+        bar_sum += rk / static_cast<double>(k + 1);
+        if (k >= 1 && std::fabs(rk) > kConsistencyTol)
+          return bad("degree-" + std::to_string(k) + " row sum nonzero at stage " +
+                     std::to_string(i));
+      }
+      if (std::fabs(bar_sum - dc) > kConsistencyTol)
+        return bad("row integral != dc at stage " + std::to_string(i));
+    }
+  }
+  for (int i = 0; i < s; ++i) cp.fI_ref[i] = cp.fE_ref[i] = false;
+  for (int k = 0; k < cp.ndeg_g; ++k)
+    for (int i = 0; i < s; ++i)
+      for (int j = 0; j < i; ++j)
+        if (cp.G(k, i, j) != 0.0) cp.fI_ref[j] = true;
+  for (int k = 0; k < cp.ndeg_o; ++k)
+    for (int i = 0; i < s; ++i)
+      for (int j = 0; j < i; ++j)
+        if (cp.W(k, i, j) != 0.0) cp.fE_ref[j] = true;
+  for (int i = 0; i < s; ++i) cp.eval_at[i] = cp.fE_ref[i];
+  if (!has_g && has_o) cp.eval_at[s - 1] = true;  // mri.cpp:162-166
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+struct Op {
+  enum Type { SLOW = 0, COUNT_SLOW = 1, CHAIN = 2, UPDATE = 3, MISSING = 4 } type;
+  int stage = 0;
+  std::vector<int> stages;  // CHAIN
+};
+
+struct Plan {
+  std::vector<Op> ops;
+  int slot_of[kMaxStages];
+  int nslots = 0;
+};
+
+}  // namespace
+
+struct mr_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  // grid
+  bool has_grid = false;
+  int n0 = 0, n1 = 0, n2 = 0, ncomp = 0, i0 = 0, n0l = 0;
+  double length = 1.0;
+  size_t plane = 0, ncell = 0, dof = 0;
+  // method
+  bool has_coupling = false, has_table = false;
+  Coupling cp;
+  TableDev tab{};
+  int m = 1;
+  // plugins
+  int fast_kind = -1, slow_kind = -1;
+  int S = 0, R = 0;
+  double rho = 0.0;
+  ChemDev chem{};
+  double chem_flops = 0.0;
+  std::vector<void*> chem_bufs;
+  LinDev fastA{}, slowA{};
+  int order = 2, M = 1;
+  double D = 0.0;
+  double u[3] = {0, 0, 0};
+  int vel_kind = 0;
+  double* d_prof = nullptr;
+  int nmax = 0;
+  // buffers
+  double* y_state = nullptr;
+  double* y_work = nullptr;
+  std::vector<double*> slots;
+  double *send_lo = nullptr, *send_hi = nullptr, *recv_lo = nullptr, *recv_hi = nullptr;
+  size_t halo_elems = 0;
+  double *scr_in = nullptr, *scr_out = nullptr;
+  unsigned long long* d_fail = nullptr;
+  unsigned long long* h_fail = nullptr;
+  double* d_red = nullptr;  // partials + out
+  double* h_red = nullptr;
+  bool state_valid = false;
+  // comm
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  // instrumentation
+  uint64_t launches = 0;
+  bool profile = false;
+  double prof_chem = 0, prof_slow = 0, prof_other = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  int fail_mri = -1, fail_sub = -1, fail_inner = -1;
+  bool graphs = true;
+};
+
+namespace {
+
+int set_err(mr_ctx* c, int code, const std::string& msg)
+{
+  if (c) c->err = msg;
+  return code;
+}
+
+#define MR_CUDA_TRY(ctx, call)                                                            \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return set_err(ctx, MR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+#define MR_NCCL_TRY(ctx, call)                                                            \
+  do {                                                                                     \
+    ncclResult_t r_ = (call);                                                              \
+    if (r_ != ncclSuccess)                                                                 \
+      return set_err(ctx, MR_CUDA, std::string(#call) + ": " + ncclGetErrorString(r_));    \
+  } while (0)
+
+void free_dev(void*& p)
+{
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+template <class T>
+void free_dev_t(T*& p)
+{
+  void* q = p;
+  free_dev(q);
+  p = nullptr;
+}
+
+void free_state(mr_ctx* c)
+{
+  free_dev_t(c->y_state);
+  free_dev_t(c->y_work);
+  for (auto& p : c->slots) free_dev_t(p);
+  c->slots.clear();
+  free_dev_t(c->send_lo);
+  free_dev_t(c->send_hi);
+  free_dev_t(c->recv_lo);
+  free_dev_t(c->recv_hi);
+  free_dev_t(c->scr_in);
+  free_dev_t(c->scr_out);
+  c->halo_elems = 0;
+  c->state_valid = false;
+}
+
+int ensure_state(mr_ctx* c)
+{
+  if (!c->has_grid) return set_err(c, MR_CONTRACT, "grid not set (mr_grid_set)");
+  if (!c->y_state) {
+    MR_CUDA_TRY(c, cudaMalloc(&c->y_state, c->dof * sizeof(double)));
+    MR_CUDA_TRY(c, cudaMemsetAsync(c->y_state, 0, c->dof * sizeof(double), c->stream));
+  }
+  if (!c->y_work) MR_CUDA_TRY(c, cudaMalloc(&c->y_work, c->dof * sizeof(double)));
+  return MR_OK;
+}
+
+int ensure_slots(mr_ctx* c, int n)
+{
+  while ((int)c->slots.size() < n) {
+    double* p = nullptr;
+    MR_CUDA_TRY(c, cudaMalloc(&p, c->dof * sizeof(double)));
+    c->slots.push_back(p);
+  }
+  return MR_OK;
+}
+
+int ensure_halo(mr_ctx* c)
+{
+  const size_t need = (size_t)c->ncomp * c->M * c->plane;
+  if (c->halo_elems == need) return MR_OK;
+  free_dev_t(c->send_lo);
+  free_dev_t(c->send_hi);
+  free_dev_t(c->recv_lo);
+  free_dev_t(c->recv_hi);
+  MR_CUDA_TRY(c, cudaMalloc(&c->send_lo, need * sizeof(double)));
+  MR_CUDA_TRY(c, cudaMalloc(&c->send_hi, need * sizeof(double)));
+  if (c->nranks > 1) {
+    MR_CUDA_TRY(c, cudaMalloc(&c->recv_lo, need * sizeof(double)));
+    MR_CUDA_TRY(c, cudaMalloc(&c->recv_hi, need * sizeof(double)));
+  }
+  c->halo_elems = need;
+  return MR_OK;
+}
+
+bool fast_present(const mr_ctx* c) { return c->fast_kind != FK_NONE; }
+bool slow_present(const mr_ctx* c) { return c->slow_kind != SK_NONE; }
+
+int check_ready(mr_ctx* c)
+{
+  if (!c->has_grid) return set_err(c, MR_CONTRACT, "grid not set (mr_grid_set)");
+  if (!c->has_coupling) return set_err(c, MR_CONTRACT, "coupling not loaded");
+  if (!c->has_table) return set_err(c, MR_CONTRACT, "fast table not loaded");
+  if (c->fast_kind < 0 || c->slow_kind < 0)
+    return set_err(c, MR_CONTRACT, "PartitionedSystem: fast/slow plugins not configured");
+  if (c->fast_kind == FK_NONE && c->slow_kind == SK_NONE)
+    return set_err(c, MR_CONTRACT, "PartitionedSystem: at least one partition required");
+  if (c->cp.implicit)
+    return set_err(c, MR_CONTRACT,
+                   "mri_step: coupling needs f_implicit (IMEX stages are not on the explicit "
+                   "device path yet)");
+  if (c->fast_kind == FK_CHEM && c->ncomp != c->S + 1)
+    return set_err(c, MR_CONTRACT, "chemistry plugin needs n_comp == S + 1");
+  if ((c->fast_kind == FK_LINEAR && c->fastA.n != c->ncomp) ||
+      (c->slow_kind == SK_LINEAR && c->slowA.n != c->ncomp))
+    return set_err(c, MR_CONTRACT, "linear plugin size != n_comp");
+  if (c->slow_kind == SK_STENCIL && c->n0l < c->M)
+    return set_err(c, MR_CONTRACT, "slab thinner than the stencil ghost width");
+  return MR_OK;
+}
+
+Plan build_plan(const mr_ctx* c)
+{
+  const Coupling& cp = c->cp;
+  const int s = cp.s;
+  Plan p;
+  for (int i = 0; i < kMaxStages; ++i) p.slot_of[i] = -1;
+  const bool slow = slow_present(c);
+  for (int j = 0; j < s; ++j)
+    if (slow && cp.eval_at[j] && cp.fE_ref[j]) p.slot_of[j] = p.nslots++;
+  auto slow_op = [&](int j) {
+    if (!slow || !cp.eval_at[j]) return;
+    Op o;
+    o.type = p.slot_of[j] >= 0 ? Op::SLOW : Op::COUNT_SLOW;  // unreferenced: count only
+    o.stage = j;
+    p.ops.push_back(o);
+  };
+  slow_op(0);
+  std::vector<int> run;
+  auto flush = [&]() {
+    if (run.empty()) return;
+    bool has_ivp = false;
+    for (int i : run) has_ivp |= cp.kind[i] == MR_STAGE_FAST_IVP;
+    if (!has_ivp) {
+      for (int i : run) {
+        Op o;
+        o.type = Op::UPDATE;
+        o.stage = i;
+        p.ops.push_back(o);
+      }
+    } else {
+      for (size_t a = 0; a < run.size(); a += MR_MAXCHAIN) {
+        Op o;
+        o.type = Op::CHAIN;
+        for (size_t b = a; b < std::min(run.size(), a + MR_MAXCHAIN); ++b) o.stages.push_back(run[b]);
+        p.ops.push_back(o);
+      }
+    }
+    run.clear();
+  };
+  for (int i = 1; i < s; ++i) {
+    // a stage referencing a slow value that is never evaluated: the reference
+    // fails inside build_forcing / axpy_into at that stage (mri.cpp:288-296)
+    bool missing = false;
+    for (int j = 0; j < i; ++j) {
+      bool refd = false;
+      if (cp.kind[i] == MR_STAGE_FAST_IVP) {
+        for (int k = 0; k < cp.ndeg_o; ++k) refd |= cp.W(k, i, j) != 0.0;
+      } else {
+        refd = cp.wbar[i][j] != 0.0;
+      }
+      if (refd && p.slot_of[j] < 0) missing = true;
+    }
+    if (missing) {
+      flush();
+      Op o;
+      o.type = Op::MISSING;
+      o.stage = i;
+      p.ops.push_back(o);
+      return p;
+    }
+    run.push_back(i);
+    if ((slow && cp.eval_at[i]) || i == s - 1) {
+      flush();
+      slow_op(i);
+    }
+  }
+  return p;
+}
+
+// per-stage IVP schedule (mri.cpp:358-377)
+struct IvpSched {
+  int n_sub;
+  double t_start, span, h_sub, dc;
+};
+
+IvpSched ivp_sched(const mr_ctx* c, int i, double t, double H)
+{
+  const Coupling& cp = c->cp;
+  IvpSched r;
+  r.dc = cp.c[i] - cp.c[i - 1];
+  r.span = r.dc * H;
+  r.n_sub = static_cast<int>(std::max(1L, std::lround(static_cast<double>(c->m) * r.dc)));
+  r.t_start = t + cp.c[i - 1] * H;
+  r.h_sub = r.span / r.n_sub;
+  return r;
+}
+
+int ndeg_of(const mr_ctx* c) { return std::max(c->cp.degrees(), 1); }
+
+void fill_chain_stage(const mr_ctx* c, int i, double t, double H, const Plan& p,
+                      ChainStageDev& st)
+{
+  const Coupling& cp = c->cp;
+  std::memset(&st, 0, sizeof(st));
+  st.mri_stage = i;
+  if (cp.kind[i] == MR_STAGE_FAST_IVP) {
+    const IvpSched sc = ivp_sched(c, i, t, H);
+    st.kind = 0;
+    st.n_sub = sc.n_sub;
+    st.t_start = sc.t_start;
+    st.span = sc.span;
+    st.h_sub = sc.h_sub;
+    for (int j = 0; j < i; ++j) {
+      bool refd = false;
+      for (int k = 0; k < cp.ndeg_o; ++k) refd |= cp.W(k, i, j) != 0.0;
+      if (!refd) continue;
+      const int r = st.nref++;
+      st.ref_slot[r] = p.slot_of[j];
+      for (int k = 0; k < MR_MAXDEG; ++k)
+        st.coef[k][r] = k < cp.ndeg_o ? cp.W(k, i, j) / sc.dc : 0.0;
+    }
+  } else {
+    st.kind = 2;
+    for (int j = 0; j < i; ++j) {
+      if (cp.wbar[i][j] == 0.0) continue;
+      const int r = st.nref++;
+      st.ref_slot[r] = p.slot_of[j];
+      st.coef[0][r] = H * cp.wbar[i][j];
+    }
+  }
+}
+
+cudaEvent_t pool_event(mr_ctx* c, size_t idx)
+{
+  while (c->ev_pool.size() <= idx) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[idx];
+}
+
+// ---------------------------------------------------------------------------
+// halo exchange for the stencil: fills halo pointers of every context
+// ---------------------------------------------------------------------------
+int exchange_halos(mr_ctx** cs, int n, const double* const* ycur, const double** lo,
+                   const double** hi, cudaStream_t st)
+{
+  for (int r = 0; r < n; ++r) {
+    mr_ctx* c = cs[r];
+    int rc = ensure_halo(c);
+    if (rc) return rc;
+    MR_CUDA_TRY(c, launch_halo_pack(ycur[r], c->send_lo, c->send_hi, c->ncomp, c->n0l, c->plane,
+                                    c->M, st));
+    c->launches++;
+  }
+  if (n == 1 && cs[0]->nranks == 1) {  // periodic single slab: own planes wrap around
+    lo[0] = cs[0]->send_hi;
+    hi[0] = cs[0]->send_lo;
+    return MR_OK;
+  }
+  if (n == 1) {  // NCCL ring of slabs
+    mr_ctx* c = cs[0];
+    const int left = (c->rank - 1 + c->nranks) % c->nranks;
+    const int right = (c->rank + 1) % c->nranks;
+    MR_NCCL_TRY(c, ncclGroupStart());
+    MR_NCCL_TRY(c, ncclSend(c->send_lo, c->halo_elems, ncclDouble, left, c->comm, st));
+    MR_NCCL_TRY(c, ncclRecv(c->recv_hi, c->halo_elems, ncclDouble, right, c->comm, st));
+    MR_NCCL_TRY(c, ncclSend(c->send_hi, c->halo_elems, ncclDouble, right, c->comm, st));
+    MR_NCCL_TRY(c, ncclRecv(c->recv_lo, c->halo_elems, ncclDouble, left, c->comm, st));
+    MR_NCCL_TRY(c, ncclGroupEnd());
+    lo[0] = c->recv_lo;
+    hi[0] = c->recv_hi;
+    return MR_OK;
+  }
+  // in-process virtual ranks on one device: device-to-device copies
+  for (int r = 0; r < n; ++r) {
+    mr_ctx* c = cs[r];
+    if (!c->recv_lo) {
+      MR_CUDA_TRY(c, cudaMalloc(&c->recv_lo, c->halo_elems * sizeof(double)));
+      MR_CUDA_TRY(c, cudaMalloc(&c->recv_hi, c->halo_elems * sizeof(double)));
+    }
+  }
+  for (int r = 0; r < n; ++r) {
+    mr_ctx* c = cs[r];
+    mr_ctx* L = cs[(r - 1 + n) % n];
+    mr_ctx* Rr = cs[(r + 1) % n];
+    MR_CUDA_TRY(c, cudaMemcpyAsync(c->recv_lo, L->send_hi, c->halo_elems * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, st));
+    MR_CUDA_TRY(c, cudaMemcpyAsync(c->recv_hi, Rr->send_lo, c->halo_elems * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, st));
+    lo[r] = c->recv_lo;
+    hi[r] = c->recv_hi;
+  }
+  return MR_OK;
+}
+
+StencilArgs stencil_args(const mr_ctx* c, const double* y, double* out, const double* lo,
+                         const double* hi)
+{
+  StencilArgs a{};
+  a.y = y;
+  a.out = out;
+  a.halo_lo = lo;
+  a.halo_hi = hi;
+  a.n0l = c->n0l;
+  a.n1 = c->n1;
+  a.n2 = c->n2;
+  a.ncomp = c->ncomp;
+  a.M = c->M;
+  a.i0 = c->i0;
+  for (int i = 0; i < 5; ++i) a.a[i] = a.b[i] = 0.0;
+  if (c->order == 2) {
+    a.a[1] = 1.0 / 2.0;
+    a.b[0] = -2.0; a.b[1] = 1.0;
+  } else if (c->order == 4) {
+    a.a[1] = 2.0 / 3.0; a.a[2] = -1.0 / 12.0;
+    a.b[0] = -5.0 / 2.0; a.b[1] = 4.0 / 3.0; a.b[2] = -1.0 / 12.0;
+  } else {
+    a.a[1] = 4.0 / 5.0; a.a[2] = -1.0 / 5.0; a.a[3] = 4.0 / 105.0; a.a[4] = -1.0 / 280.0;
+    a.b[0] = -205.0 / 72.0; a.b[1] = 8.0 / 5.0; a.b[2] = -1.0 / 5.0; a.b[3] = 8.0 / 315.0;
+    a.b[4] = -1.0 / 560.0;
+  }
+  const int ng[3] = {c->n0, c->n1, c->n2};
+  for (int d = 0; d < 3; ++d) {
+    const double dx = c->length / ng[d];
+    a.inv_dx[d] = 1.0 / dx;
+    a.inv_dx2[d] = 1.0 / (dx * dx);
+  }
+  a.D = c->D;
+  a.vel_kind = c->vel_kind;
+  for (int d = 0; d < 3; ++d) a.u[d] = c->u[d];
+  a.prof = c->d_prof;
+  a.nmax = c->nmax;
+  return a;
+}
+
+// slow RHS of every context's current state into `outs`
+int eval_slow(mr_ctx** cs, int n, const double* const* ycur, double* const* outs,
+              cudaStream_t st)
+{
+  if (cs[0]->slow_kind == SK_LINEAR) {
+    for (int r = 0; r < n; ++r) {
+      MR_CUDA_TRY(cs[r], launch_slow_linear(ycur[r], outs[r], cs[r]->ncell, cs[r]->slowA, st));
+      cs[r]->launches++;
+    }
+    return MR_OK;
+  }
+  std::vector<const double*> lo(n), hi(n);
+  int rc = exchange_halos(cs, n, ycur, lo.data(), hi.data(), st);
+  if (rc) return rc;
+  for (int r = 0; r < n; ++r) {
+    MR_CUDA_TRY(cs[r], launch_stencil(stencil_args(cs[r], ycur[r], outs[r], lo[r], hi[r]), st));
+    cs[r]->launches++;
+  }
+  return MR_OK;
+}
+
+void add_counts_full(const mr_ctx* c, const Plan& p, double t, double H, uint64_t* cnt)
+{
+  for (const Op& o : p.ops) {
+    if (o.type == Op::SLOW || o.type == Op::COUNT_SLOW) cnt[MR_CNT_EXPLICIT_EVALS]++;
+    if (o.type == Op::CHAIN)
+      for (int i : o.stages)
+        if (c->cp.kind[i] == MR_STAGE_FAST_IVP) {
+          if (fast_present(c))
+            cnt[MR_CNT_FAST_EVALS] += (uint64_t)ivp_sched(c, i, t, H).n_sub * c->tab.s;
+          cnt[MR_CNT_FAST_IVPS]++;
+        }
+  }
+}
+
+// counts up to a failure at (stage, sub, inner) -- what the reference's
+// by-reference EvalCounters hold when mri_step throws
+void add_counts_partial(const mr_ctx* c, const Plan& p, double t, double H, int fs, int fsub,
+                        int finner, uint64_t* cnt)
+{
+  for (const Op& o : p.ops) {
+    if ((o.type == Op::SLOW || o.type == Op::COUNT_SLOW) && o.stage < fs)
+      cnt[MR_CNT_EXPLICIT_EVALS]++;
+    if (o.type == Op::CHAIN)
+      for (int i : o.stages) {
+        if (c->cp.kind[i] != MR_STAGE_FAST_IVP || i > fs) continue;
+        const int ns = ivp_sched(c, i, t, H).n_sub;
+        if (i < fs) {
+          if (fast_present(c)) cnt[MR_CNT_FAST_EVALS] += (uint64_t)ns * c->tab.s;
+          cnt[MR_CNT_FAST_IVPS]++;
+        } else if (fast_present(c)) {
+          cnt[MR_CNT_FAST_EVALS] += (uint64_t)fsub * c->tab.s + (uint64_t)finner;
+        }
+      }
+  }
+}
+
+// One slow step over a domain of slab contexts sharing a device stream (n > 1)
+// or one context (n == 1, possibly an NCCL rank).
+int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int* fail_stage)
+{
+  mr_ctx* c0 = cs[0];
+  if (fail_stage) *fail_stage = -1;
+  if (!(H > 0.0)) return set_err(c0, MR_CONTRACT, "mri_step: H must be positive");
+  for (int r = 0; r < n; ++r) {
+    int rc = check_ready(cs[r]);
+    if (rc) return rc;
+    rc = ensure_state(cs[r]);
+    if (rc) return rc;
+  }
+  const Plan plan = build_plan(c0);
+  for (int r = 0; r < n; ++r) {
+    int rc = ensure_slots(cs[r], plan.nslots);
+    if (rc) return rc;
+  }
+  cudaStream_t st = c0->stream;
+  ChainCfg cfg;
+  if (chain_pick(&cfg, c0->fast_kind, c0->ncomp, c0->S, c0->R, c0->tab.s, ndeg_of(c0)))
+    return set_err(c0, MR_CONTRACT, "unsupported component count / table for the fused IVP kernel");
+  for (int r = 0; r < n; ++r)
+    MR_CUDA_TRY(cs[r], cudaMemsetAsync(cs[r]->d_fail, 0xFF, sizeof(unsigned long long), st));
+
+  std::vector<const double*> ycur(n);
+  std::vector<double*> outs(n);
+  for (int r = 0; r < n; ++r) ycur[r] = cs[r]->y_state;
+  bool on_work = false;
+  size_t ev = 0;
+  std::vector<std::pair<int, size_t>> timed;  // (class, event index)
+  int missing_stage = -1;
+
+  for (const Op& o : plan.ops) {
+    if (o.type == Op::COUNT_SLOW) continue;
+    if (o.type == Op::MISSING) {
+      missing_stage = o.stage;
+      break;
+    }
+    const int cls = o.type == Op::CHAIN ? 0 : (o.type == Op::SLOW ? 1 : 2);
+    if (c0->profile) {
+      cudaEventRecord(pool_event(c0, ev), st);
+      timed.push_back({cls, ev});
+      ev += 2;
+    }
+    if (o.type == Op::SLOW) {
+      for (int r = 0; r < n; ++r) outs[r] = cs[r]->slots[plan.slot_of[o.stage]];
+      int rc = eval_slow(cs, n, ycur.data(), outs.data(), st);
+      if (rc) return rc;
+    } else if (o.type == Op::UPDATE) {
+      for (int r = 0; r < n; ++r) {
+        mr_ctx* c = cs[r];
+        ChainStageDev sd;
+        fill_chain_stage(c, o.stage, t, H, plan, sd);
+        const double* f[MR_MAXREF];
+        for (int q = 0; q < sd.nref; ++q) f[q] = c->slots[sd.ref_slot[q]];
+        MR_CUDA_TRY(c, launch_update(ycur[r], c->y_work, sd.nref, f, sd.coef[0], c->dof, o.stage,
+                                     c->d_fail, st));
+        c->launches++;
+        ycur[r] = c->y_work;
+      }
+      on_work = true;
+    } else {  // CHAIN
+      for (int r = 0; r < n; ++r) {
+        mr_ctx* c = cs[r];
+        ChainArgs a;
+        std::memset(&a, 0, sizeof(a));
+        a.nst = (int)o.stages.size();
+        a.ndeg = ndeg_of(c);
+        for (int q = 0; q < a.nst; ++q) fill_chain_stage(c, o.stages[q], t, H, plan, a.st[q]);
+        a.tab = c->tab;
+        a.y_in = ycur[r];
+        a.y_out = c->y_work;
+        for (int q = 0; q < (int)c->slots.size() && q < MR_MAXSLOT; ++q) a.fE[q] = c->slots[q];
+        a.ncell = c->ncell;
+        a.ncomp = c->ncomp;
+        a.fail = c->d_fail;
+        MR_CUDA_TRY(c, launch_chain(cfg, a, c->chem, c->fastA, st));
+        c->launches++;
+        ycur[r] = c->y_work;
+      }
+      on_work = true;
+    }
+    if (c0->profile) cudaEventRecord(pool_event(c0, timed.back().second + 1), st);
+  }
+  (void)on_work;
+
+  // combine failure keys (min over slabs / ranks)
+  unsigned long long key = MR_NO_FAIL;
+  if (n == 1 && c0->nranks > 1) {
+    MR_NCCL_TRY(c0, ncclAllReduce(c0->d_fail, c0->d_fail, 1, ncclUint64, ncclMin, c0->comm, st));
+  }
+  for (int r = 0; r < n; ++r) {
+    MR_CUDA_TRY(cs[r], cudaMemcpyAsync(cs[r]->h_fail, cs[r]->d_fail, sizeof(unsigned long long),
+                                       cudaMemcpyDeviceToHost, st));
+  }
+  MR_CUDA_TRY(c0, cudaStreamSynchronize(st));
+  for (int r = 0; r < n; ++r) key = std::min(key, *cs[r]->h_fail);
+
+  if (c0->profile) {
+    c0->prof_chem = c0->prof_slow = c0->prof_other = 0.0;
+    for (auto& tv : timed) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c0->ev_pool[tv.second], c0->ev_pool[tv.second + 1]);
+      (tv.first == 0 ? c0->prof_chem : tv.first == 1 ? c0->prof_slow : c0->prof_other) += ms;
+    }
+  }
+
+  if (missing_stage >= 0 && key == MR_NO_FAIL) {
+    // stages before the missing reference ran; count them, report the failure
+    const Coupling& cp = c0->cp;
+    uint64_t part[8] = {};
+    add_counts_partial(c0, plan, t, H, missing_stage, 0, 0, part);
+    if (counters)
+      for (int q = 0; q < 8; ++q) counters[q] += part[q];
+    for (int r = 0; r < n; ++r) {
+      cs[r]->fail_mri = missing_stage;
+      cs[r]->fail_sub = cs[r]->fail_inner = -1;
+    }
+    if (cp.kind[missing_stage] == MR_STAGE_FAST_IVP) {
+      if (fail_stage) *fail_stage = missing_stage;
+      return set_err(c0, MR_INTEGRATION,
+                     "build_forcing: missing explicit value at stage " + std::to_string(missing_stage));
+    }
+    return set_err(c0, MR_CONTRACT, "axpy_into: length mismatch");
+  }
+
+  if (key != MR_NO_FAIL) {
+    const int fs = (int)(key >> 40);
+    const int fsub = (int)((key >> 8) & 0xFFFFFFFFull);
+    const int finner = (int)(key & 0xFFull);
+    uint64_t part[8] = {};
+    const bool ivp = c0->cp.kind[fs] == MR_STAGE_FAST_IVP;
+    add_counts_partial(c0, plan, t, H, fs, ivp ? fsub : 0, ivp ? finner : 0, part);
+    if (counters)
+      for (int q = 0; q < 8; ++q) counters[q] += part[q];
+    for (int r = 0; r < n; ++r) {
+      cs[r]->fail_mri = fs;
+      cs[r]->fail_sub = ivp ? fsub : -1;
+      cs[r]->fail_inner = ivp ? finner : -1;
+    }
+    if (fail_stage) *fail_stage = ivp ? finner : fs;
+    if (ivp)
+      return set_err(c0, MR_INTEGRATION,
+                     finner == c0->tab.s ? "erk_step: non-finite result"
+                                         : "erk_step: non-finite stage value");
+    return set_err(c0, MR_INTEGRATION, "mri_step: non-finite state at stage " + std::to_string(fs));
+  }
+  if (counters) add_counts_full(c0, plan, t, H, counters);
+  for (int r = 0; r < n; ++r) {
+    mr_ctx* c = cs[r];
+    if (ycur[r] == c->y_work) std::swap(c->y_state, c->y_work);
+    c->fail_mri = c->fail_sub = c->fail_inner = -1;
+  }
+  return MR_OK;
+}
+
+int read_coupling_text(const char* text, Coupling& cp, std::string& err)
+{
+  std::istringstream in(text);
+  std::string magic, version, name, sf, df;
+  in >> magic >> version >> name >> sf >> df;
+  if (magic != "mri-coupling" || version != "v1" || sf.rfind("s=", 0) != 0 ||
+      df.rfind("degrees=", 0) != 0) {
+    err = "import_coupling: bad header";
+    return MR_CONTRACT;
+  }
+  cp = Coupling();
+  cp.name = name;
+  cp.s = std::atoi(sf.c_str() + 2);
+  const int d = std::atoi(df.c_str() + 8);
+  if (cp.s < 2 || d < 1 || cp.s > kMaxStages) {
+    err = "import_coupling: bad dimensions";
+    return MR_CONTRACT;
+  }
+  for (int i = 0; i < cp.s; ++i) in >> cp.c[i];
+  for (int i = 0; i < cp.s; ++i) {
+    std::string tok;
+    in >> tok;
+    if (tok == "fast-ivp") cp.kind[i] = MR_STAGE_FAST_IVP;
+    else if (tok == "implicit-solve") cp.kind[i] = MR_STAGE_IMPLICIT_SOLVE;
+    else if (tok == "explicit-update") cp.kind[i] = MR_STAGE_EXPLICIT_UPDATE;
+    else {
+      err = "import_coupling: unknown stage kind '" + tok + "'";
+      return MR_CONTRACT;
+    }
+  }
+  cp.ndeg_g = cp.ndeg_o = d;
+  cp.gamma.assign((size_t)d * cp.s * cp.s, 0.0);
+  cp.omega.assign((size_t)d * cp.s * cp.s, 0.0);
+  for (auto& v : cp.gamma) in >> v;
+  for (auto& v : cp.omega) in >> v;
+  if (!in) {
+    err = "import_coupling: truncated input";
+    return MR_CONTRACT;
+  }
+  return finalize(cp, err) ? MR_OK : MR_CONTRACT;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+int mr_version(void) { return 1; }
+
+int mr_ctx_create(int device, mr_ctx** out)
+{
+  if (!out) return MR_CONTRACT;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return MR_CUDA;
+  if (device < 0 || device >= ndev) return MR_CONTRACT;
+  if (cudaSetDevice(device) != cudaSuccess) return MR_CUDA;
+  mr_ctx* c = new mr_ctx();
+  c->device = device;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&c->d_fail, sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMallocHost(&c->h_fail, sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&c->d_red, sizeof(double) * (reduce_blocks() + 8)) != cudaSuccess ||
+      cudaMallocHost(&c->h_red, sizeof(double) * 8) != cudaSuccess) {
+    delete c;
+    return MR_CUDA;
+  }
+  *out = c;
+  return MR_OK;
+}
+
+void mr_ctx_destroy(mr_ctx* c)
+{
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  free_state(c);
+  for (void*& p : c->chem_bufs) free_dev(p);
+  free_dev_t(c->d_prof);
+  free_dev_t(c->d_fail);
+  free_dev_t(c->d_red);
+  if (c->h_fail) cudaFreeHost(c->h_fail);
+  if (c->h_red) cudaFreeHost(c->h_red);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->comm) ncclCommDestroy(c->comm);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* mr_last_error(const mr_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int mr_grid_set(mr_ctx* c, int n0, int n1, int n2, int n_comp, double length, int i0, int n0_local)
+{
+  if (!c) return MR_CONTRACT;
+  if (n0 < 1 || n1 < 1 || n2 < 1 || n_comp < 1 || !(length > 0.0) || i0 < 0 || n0_local < 1 ||
+      i0 + n0_local > n0)
+    return set_err(c, MR_CONTRACT, "mr_grid_set: bad grid");
+  cudaSetDevice(c->device);
+  free_state(c);
+  c->n0 = n0; c->n1 = n1; c->n2 = n2; c->ncomp = n_comp; c->length = length;
+  c->i0 = i0; c->n0l = n0_local;
+  c->plane = (size_t)n1 * n2;
+  c->ncell = c->plane * n0_local;
+  c->dof = c->ncell * n_comp;
+  c->has_grid = true;
+  return MR_OK;
+}
+
+int mr_coupling_load(mr_ctx* c, int s, int n_deg, const double* cc, const int* kind,
+                     const double* gamma, const double* omega)
+{
+  if (!c || !cc || !kind || s < 2 || s > kMaxStages || n_deg < 1 || n_deg > 8)
+    return set_err(c, MR_CONTRACT, "mr_coupling_load: bad arguments");
+  Coupling cp;
+  cp.name = "loaded";
+  cp.s = s;
+  cp.ndeg_g = gamma ? n_deg : 0;
+  cp.ndeg_o = omega ? n_deg : 0;
+  for (int i = 0; i < s; ++i) {
+    cp.c[i] = cc[i];
+    cp.kind[i] = kind[i];
+  }
+  if (gamma) cp.gamma.assign(gamma, gamma + (size_t)n_deg * s * s);
+  if (omega) cp.omega.assign(omega, omega + (size_t)n_deg * s * s);
+  std::string err;
+  if (!finalize(cp, err)) return set_err(c, MR_CONTRACT, err);
+  if (std::max(cp.degrees(), 1) > MR_MAXDEG)
+    return set_err(c, MR_CONTRACT, "forcing polynomial degree > 2 not supported");
+  c->cp = cp;
+  c->has_coupling = true;
+  return MR_OK;
+}
+
+int mr_coupling_load_text(mr_ctx* c, const char* text)
+{
+  if (!c || !text) return MR_CONTRACT;
+  Coupling cp;
+  std::string err;
+  int rc = read_coupling_text(text, cp, err);
+  if (rc) return set_err(c, rc, err);
+  if (std::max(cp.degrees(), 1) > MR_MAXDEG)
+    return set_err(c, MR_CONTRACT, "forcing polynomial degree > 2 not supported");
+  c->cp = cp;
+  c->has_coupling = true;
+  return MR_OK;
+}
+
+int mr_table_load(mr_ctx* c, int s, const double* A, const double* b, const double* cc)
+{
+  if (!c || !A || !b || !cc || s < 1 || s > MR_MAXS)
+    return set_err(c, MR_CONTRACT, "mr_table_load: bad arguments");
+  TableDev t{};
+  t.s = s;
+  for (int i = 0; i < s; ++i) {
+    for (int j = 0; j < s; ++j) {
+      t.A[i][j] = A[i * s + j];
+      if (j >= i && A[i * s + j] != 0.0)
+        return set_err(c, MR_CONTRACT, "erk_step: table must be explicit");
+    }
+    t.b[i] = b[i];
+    t.c[i] = cc[i];
+  }
+  c->tab = t;
+  c->has_table = true;
+  return MR_OK;
+}
+
+int mr_set_substeps(mr_ctx* c, int m)
+{
+  if (!c || m < 1) return set_err(c, MR_CONTRACT, "m must be >= 1");
+  c->m = m;
+  return MR_OK;
+}
+
+int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species,
+                      const double* reactions, const int* rspecies)
+{
+  if (!c || S < 1 || R < 1 || !(rho > 0.0) || !species || !reactions || !rspecies)
+    return set_err(c, MR_CONTRACT, "mr_fast_chemistry: bad arguments");
+  cudaSetDevice(c->device);
+  for (void*& p : c->chem_bufs) free_dev(p);
+  c->chem_bufs.clear();
+  const int Sp = (S + 1 + 31) / 32 * 32;
+  std::vector<double> sp(9 * (size_t)Sp, 0.0);
+  for (int k = 0; k < S; ++k) {
+    const double W = species[5 * k], a = species[5 * k + 1], b = species[5 * k + 2];
+    const double h0 = species[5 * k + 3], s0 = species[5 * k + 4];
+    const double rW = kRu / W;
+    sp[0 * Sp + k] = h0;
+    sp[1 * Sp + k] = a;
+    sp[2 * Sp + k] = 0.5 * b;
+    sp[3 * Sp + k] = s0;
+    sp[4 * Sp + k] = rho / W;
+    sp[5 * Sp + k] = W / rho;
+    sp[6 * Sp + k] = rW * h0;
+    sp[7 * Sp + k] = rW * (a - 1.0);
+    sp[8 * Sp + k] = rW * (0.5 * b);
+  }
+  std::vector<double4> rx(R);
+  std::vector<int4> rs(R);
+  std::vector<int> cnt(S + 1, 0);
+  for (int j = 0; j < R; ++j) {
+    int q[4];
+    for (int t = 0; t < 4; ++t) {
+      q[t] = rspecies[4 * j + t];
+      if (q[t] >= S || (q[t] < 0 && (t == 0 || t == 2)))
+        return set_err(c, MR_CONTRACT, "mr_fast_chemistry: bad species index");
+      if (q[t] >= 0) cnt[q[t] + 1]++;
+    }
+    const int nr = 1 + (q[1] >= 0), np = 1 + (q[3] >= 0);
+    rx[j] = make_double4(reactions[3 * j], reactions[3 * j + 1], reactions[3 * j + 2],
+                         (double)(np - nr));
+    rs[j] = make_int4(q[0], q[1] < 0 ? S : q[1], q[2], q[3] < 0 ? S : q[3]);
+  }
+  for (int k = 0; k < S; ++k) cnt[k + 1] += cnt[k];
+  std::vector<int> ent(std::max(cnt[S], 1));
+  std::vector<int> fill(S, 0);
+  for (int j = 0; j < R; ++j)
+    for (int t = 0; t < 4; ++t) {
+      const int k = rspecies[4 * j + t];
+      if (k < 0) continue;
+      ent[cnt[k] + fill[k]++] = 2 * j + (t >= 2 ? 1 : 0);
+    }
+  auto up = [&](const void* h, size_t bytes) -> void* {
+    void* d = nullptr;
+    if (cudaMalloc(&d, bytes) != cudaSuccess) return nullptr;
+    cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice);
+    c->chem_bufs.push_back(d);
+    return d;
+  };
+  ChemDev ch{};
+  ch.S = S;
+  ch.R = R;
+  ch.Spad = Sp;
+  ch.sp = (const double*)up(sp.data(), sp.size() * sizeof(double));
+  ch.rxn = (const double4*)up(rx.data(), rx.size() * sizeof(double4));
+  ch.rsp = (const int4*)up(rs.data(), rs.size() * sizeof(int4));
+  ch.csr_off = (const int*)up(cnt.data(), cnt.size() * sizeof(int));
+  ch.csr_ent = (const int*)up(ent.data(), ent.size() * sizeof(int));
+  ch.RuP = kRu / kPatm;
+  if (!ch.sp || !ch.rxn || !ch.rsp || !ch.csr_off || !ch.csr_ent)
+    return set_err(c, MR_CUDA, "mr_fast_chemistry: device allocation failed");
+  c->chem = ch;
+  c->S = S;
+  c->R = R;
+  c->rho = rho;
+  c->fast_kind = FK_CHEM;
+  // fp64 work per RHS evaluation: FMA = 2, +-*/ = 1,
+  // exp = log = 20 (DFMA-equivalents of the libdevice sequence, profiles/)
+  const double ce = 20.0;
+  double f = 0.0;
+  f += 6.0 * S + 2.0 + 1.0 + 1.0 + 1.0 + 2.0;  // e(T) sums, closed-form root
+  f += ce + 1.0;                               // log T, 1/T
+  f += S * (6.0 + ce + 1.0 + 1.0 + 1.0);       // g, exp, 1/E, C, W/rho
+  f += 2.0;                                    // RT/P and its inverse
+  int nnz = cnt[S];
+  for (int j = 0; j < R; ++j) f += 4.0 + ce + 5.0 + 5.0;  // kf, kr, q
+  f += nnz;                                               // production sums
+  c->chem_flops = f;
+  return MR_OK;
+}
+
+int mr_fast_linear(mr_ctx* c, const double* A)
+{
+  if (!c || !A || !c->has_grid || c->ncomp > MR_MAXLIN)
+    return set_err(c, MR_CONTRACT, "mr_fast_linear: needs grid with n_comp <= 8");
+  c->fastA.n = c->ncomp;
+  for (int i = 0; i < c->ncomp * c->ncomp; ++i) c->fastA.A[i] = A[i];
+  c->fast_kind = FK_LINEAR;
+  return MR_OK;
+}
+
+int mr_fast_none(mr_ctx* c)
+{
+  if (!c) return MR_CONTRACT;
+  c->fast_kind = FK_NONE;
+  return MR_OK;
+}
+
+int mr_slow_stencil(mr_ctx* c, int order, double diffusion, const double* u, const double* prof,
+                    int nmax)
+{
+  if (!c || !c->has_grid || (order != 2 && order != 4 && order != 8) || diffusion < 0.0)
+    return set_err(c, MR_CONTRACT, "mr_slow_stencil: bad arguments (order 2/4/8, grid first)");
+  cudaSetDevice(c->device);
+  free_dev_t(c->d_prof);
+  c->order = order;
+  c->M = order / 2;
+  c->D = diffusion;
+  if (prof) {
+    if (nmax < std::max(c->n0, std::max(c->n1, c->n2)))
+      return set_err(c, MR_CONTRACT, "mr_slow_stencil: profile length < grid size");
+    MR_CUDA_TRY(c, cudaMalloc(&c->d_prof, sizeof(double) * 6 * nmax));
+    MR_CUDA_TRY(c, cudaMemcpy(c->d_prof, prof, sizeof(double) * 6 * nmax, cudaMemcpyHostToDevice));
+    c->vel_kind = 1;
+    c->nmax = nmax;
+  } else {
+    if (!u) return set_err(c, MR_CONTRACT, "mr_slow_stencil: need u or profiles");
+    for (int d = 0; d < 3; ++d) c->u[d] = u[d];
+    c->vel_kind = 0;
+  }
+  c->slow_kind = SK_STENCIL;
+  c->halo_elems = 0;
+  free_dev_t(c->send_lo);
+  free_dev_t(c->send_hi);
+  free_dev_t(c->recv_lo);
+  free_dev_t(c->recv_hi);
+  return MR_OK;
+}
+
+int mr_slow_linear(mr_ctx* c, const double* A)
+{
+  if (!c || !A || !c->has_grid || c->ncomp > MR_MAXLIN)
+    return set_err(c, MR_CONTRACT, "mr_slow_linear: needs grid with n_comp <= 8");
+  c->slowA.n = c->ncomp;
+  for (int i = 0; i < c->ncomp * c->ncomp; ++i) c->slowA.A[i] = A[i];
+  c->slow_kind = SK_LINEAR;
+  return MR_OK;
+}
+
+int mr_slow_none(mr_ctx* c)
+{
+  if (!c) return MR_CONTRACT;
+  c->slow_kind = SK_NONE;
+  return MR_OK;
+}
+
+int mr_state_upload(mr_ctx* c, const double* host)
+{
+  if (!c || !host) return MR_CONTRACT;
+  cudaSetDevice(c->device);
+  int rc = ensure_state(c);
+  if (rc) return rc;
+  MR_CUDA_TRY(c, cudaMemcpyAsync(c->y_state, host, c->dof * sizeof(double),
+                                 cudaMemcpyHostToDevice, c->stream));
+  MR_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->state_valid = true;
+  return MR_OK;
+}
+
+int mr_state_download(mr_ctx* c, double* host)
+{
+  if (!c || !host) return MR_CONTRACT;
+  if (!c->y_state) return set_err(c, MR_CONTRACT, "no state");
+  cudaSetDevice(c->device);
+  MR_CUDA_TRY(c, cudaMemcpyAsync(host, c->y_state, c->dof * sizeof(double),
+                                 cudaMemcpyDeviceToHost, c->stream));
+  MR_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MR_OK;
+}
+
+double* mr_state_device_ptr(mr_ctx* c)
+{
+  if (!c || ensure_state(c)) return nullptr;
+  return c->y_state;
+}
+
+size_t mr_state_dof(const mr_ctx* c) { return c ? c->dof : 0; }
+
+int mr_mri_step(mr_ctx* c, double t, double H, uint64_t* counters, int* fail_stage)
+{
+  if (!c) return MR_CONTRACT;
+  cudaSetDevice(c->device);
+  mr_ctx* cs[1] = {c};
+  return domain_step(cs, 1, t, H, counters, fail_stage);
+}
+
+// mri_integrate, proj/src/mri.cpp:524-540 (state unchanged on failure)
+int mr_mri_integrate(mr_ctx* c, double t0, double tf, double H, uint64_t* counters,
+                     int* fail_stage)
+{
+  if (!c) return MR_CONTRACT;
+  if (fail_stage) *fail_stage = -1;
+  if (!(tf > t0)) return set_err(c, MR_CONTRACT, "mri_integrate: tf must exceed t0");
+  cudaSetDevice(c->device);
+  int rc = ensure_state(c);
+  if (rc) return rc;
+  const long n_steps = static_cast<long>(std::ceil((tf - t0) / H - 1e-12));
+  double* backup = nullptr;
+  if (n_steps > 1) {
+    MR_CUDA_TRY(c, cudaMalloc(&backup, c->dof * sizeof(double)));
+    MR_CUDA_TRY(c, cudaMemcpyAsync(backup, c->y_state, c->dof * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, c->stream));
+  }
+  double t = t0;
+  for (long i = 0; i < n_steps; ++i) {
+    const double step = (i == n_steps - 1) ? (tf - t) : H;
+    rc = mr_mri_step(c, t, step, counters, fail_stage);
+    if (rc) break;
+    t = (i == n_steps - 1) ? tf : t0 + static_cast<double>(i + 1) * H;
+  }
+  if (backup) {
+    if (rc)
+      cudaMemcpyAsync(c->y_state, backup, c->dof * sizeof(double), cudaMemcpyDeviceToDevice,
+                      c->stream);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(backup);
+  }
+  return rc;
+}
+
+int mr_mri_step_host(mr_ctx* c, double t, double H, const double* y_in, double* y_out,
+                     uint64_t* counters, int* fail_stage)
+{
+  if (!c || !y_in || !y_out) return MR_CONTRACT;
+  cudaSetDevice(c->device);
+  int rc = ensure_state(c);
+  if (rc) return rc;
+  MR_CUDA_TRY(c, cudaMemcpyAsync(c->y_state, y_in, c->dof * sizeof(double),
+                                 cudaMemcpyHostToDevice, c->stream));
+  rc = mr_mri_step(c, t, H, counters, fail_stage);
+  if (rc) return rc;
+  MR_CUDA_TRY(c, cudaMemcpyAsync(y_out, c->y_state, c->dof * sizeof(double),
+                                 cudaMemcpyDeviceToHost, c->stream));
+  MR_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MR_OK;
+}
+
+int mr_last_failure(const mr_ctx* c, int* mri_stage, int* substep, int* inner_stage)
+{
+  if (!c) return MR_CONTRACT;
+  if (mri_stage) *mri_stage = c->fail_mri;
+  if (substep) *substep = c->fail_sub;
+  if (inner_stage) *inner_stage = c->fail_inner;
+  return MR_OK;
+}
+
+static int ensure_scratch(mr_ctx* c)
+{
+  if (!c->scr_in) MR_CUDA_TRY(c, cudaMalloc(&c->scr_in, c->dof * sizeof(double)));
+  if (!c->scr_out) MR_CUDA_TRY(c, cudaMalloc(&c->scr_out, c->dof * sizeof(double)));
+  return MR_OK;
+}
+
+int mr_fast_rhs(mr_ctx* c, double t, const double* y, double* out)
+{
+  (void)t;
+  if (!c || !y || !out) return MR_CONTRACT;
+  if (!c->has_grid || c->fast_kind < 0) return set_err(c, MR_CONTRACT, "fast plugin not set");
+  if (c->fast_kind == FK_CHEM && c->ncomp != c->S + 1)
+    return set_err(c, MR_CONTRACT, "chemistry plugin needs n_comp == S + 1");
+  cudaSetDevice(c->device);
+  int rc = ensure_scratch(c);
+  if (rc) return rc;
+  ChainCfg cfg;
+  if (chain_pick(&cfg, c->fast_kind, c->ncomp, c->S, c->R, 4, 1))
+    return set_err(c, MR_CONTRACT, "unsupported component count");
+  MR_CUDA_TRY(c, cudaMemcpyAsync(c->scr_in, y, c->dof * sizeof(double), cudaMemcpyHostToDevice,
+                                 c->stream));
+  MR_CUDA_TRY(c, launch_fast_rhs(cfg, c->scr_in, c->scr_out, c->ncell, c->ncomp, c->chem,
+                                 c->fastA, c->stream));
+  c->launches++;
+  MR_CUDA_TRY(c, cudaMemcpyAsync(out, c->scr_out, c->dof * sizeof(double), cudaMemcpyDeviceToHost,
+                                 c->stream));
+  MR_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MR_OK;
+}
+
+int mr_slow_rhs(mr_ctx* c, double t, const double* y, double* out)
+{
+  (void)t;
+  if (!c || !y || !out) return MR_CONTRACT;
+  if (!c->has_grid || c->slow_kind < 0) return set_err(c, MR_CONTRACT, "slow plugin not set");
+  if (c->slow_kind == SK_STENCIL && c->n0l < c->M)
+    return set_err(c, MR_CONTRACT, "slab thinner than the stencil ghost width");
+  cudaSetDevice(c->device);
+  int rc = ensure_scratch(c);
+  if (rc) return rc;
+  MR_CUDA_TRY(c, cudaMemcpyAsync(c->scr_in, y, c->dof * sizeof(double), cudaMemcpyHostToDevice,
+                                 c->stream));
+  if (c->slow_kind == SK_NONE) {
+    MR_CUDA_TRY(c, cudaMemsetAsync(c->scr_out, 0, c->dof * sizeof(double), c->stream));
+  } else {
+    mr_ctx* cs[1] = {c};
+    const double* yc[1] = {c->scr_in};
+    double* oc[1] = {c->scr_out};
+    rc = eval_slow(cs, 1, yc, oc, c->stream);
+    if (rc) return rc;
+  }
+  MR_CUDA_TRY(c, cudaMemcpyAsync(out, c->scr_out, c->dof * sizeof(double), cudaMemcpyDeviceToHost,
+                                 c->stream));
+  MR_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MR_OK;
+}
+
+// ---------------- reductions ----------------
+static int reduce(mr_ctx* c, int kind, const double* x, const double* w, size_t n, double* out)
+{
+  if (!c || !x || !out) return MR_CONTRACT;
+  cudaSetDevice(c->device);
+  const int nb = reduce_blocks();
+  double* part = c->d_red;
+  double* dout = c->d_red + nb;
+  MR_CUDA_TRY(c, launch_reduce(kind, x, w, n, part, nb, dout, c->stream));
+  c->launches += 2;
+  MR_CUDA_TRY(c, cudaMemcpyAsync(c->h_red, dout, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  MR_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  *out = c->h_red[0];
+  return MR_OK;
+}
+
+int mr_wrms_norm(mr_ctx* c, const double* x, const double* w, size_t n, double* out)
+{
+  if (n == 0) return set_err(c, MR_CONTRACT, "wrms_norm: empty vector");
+  if (!w) return set_err(c, MR_CONTRACT, "wrms_norm: weights required");
+  return reduce(c, RED_WRMS, x, w, n, out);
+}
+
+int mr_two_norm(mr_ctx* c, const double* x, size_t n, double* out)
+{
+  if (n == 0) { if (out) *out = 0.0; return MR_OK; }
+  return reduce(c, RED_TWO, x, nullptr, n, out);
+}
+
+int mr_dot(mr_ctx* c, const double* x, const double* y, size_t n, double* out)
+{
+  if (n == 0) { if (out) *out = 0.0; return MR_OK; }
+  if (!y) return set_err(c, MR_CONTRACT, "dot: null vector");
+  return reduce(c, RED_DOT, x, y, n, out);
+}
+
+int mr_max_norm(mr_ctx* c, const double* x, size_t n, double* out)
+{
+  if (n == 0) return set_err(c, MR_CONTRACT, "max_norm: empty vector");
+  return reduce(c, RED_MAX, x, nullptr, n, out);
+}
+
+int mr_max_norm_component(mr_ctx* c, const double* x, size_t n, size_t offset, size_t count,
+                          double* out)
+{
+  if (count == 0 || offset + count > n)
+    return set_err(c, MR_CONTRACT, "max_norm_component: bad slice");
+  return reduce(c, RED_MAX, x + offset, nullptr, count, out);
+}
+
+int mr_all_finite(mr_ctx* c, const double* x, size_t n, int* out)
+{
+  if (!out) return MR_CONTRACT;
+  if (n == 0) { *out = 1; return MR_OK; }
+  double bad = 0.0;
+  int rc = reduce(c, RED_NONFINITE, x, nullptr, n, &bad);
+  if (rc) return rc;
+  *out = bad == 0.0 ? 1 : 0;
+  return MR_OK;
+}
+
+// ---------------- multi-GPU ----------------
+int mr_nccl_unique_id(char* id128)
+{
+  if (!id128) return MR_CONTRACT;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return MR_CUDA;
+  std::memcpy(id128, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return MR_OK;
+}
+
+int mr_comm_init(mr_ctx* c, int nranks, int rank, const char* id128)
+{
+  if (!c || nranks < 1 || rank < 0 || rank >= nranks || !id128) return MR_CONTRACT;
+  cudaSetDevice(c->device);
+  if (nranks == 1) {
+    c->nranks = 1;
+    c->rank = 0;
+    return MR_OK;
+  }
+  ncclUniqueId id;
+  std::memcpy(id.internal, id128, NCCL_UNIQUE_ID_BYTES);
+  MR_NCCL_TRY(c, ncclCommInitRank(&c->comm, nranks, id, rank));
+  c->nranks = nranks;
+  c->rank = rank;
+  c->halo_elems = 0;  // reallocate halos with receive buffers
+  return MR_OK;
+}
+
+int mr_group_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int* fail_stage)
+{
+  if (!cs || n < 1) return MR_CONTRACT;
+  for (int r = 0; r < n; ++r)
+    if (!cs[r] || cs[r]->device != cs[0]->device || cs[r]->nranks != 1)
+      return set_err(cs[0], MR_CONTRACT, "mr_group_step: contexts must share one device");
+  cudaSetDevice(cs[0]->device);
+  // order all slabs on the first context's stream
+  for (int r = 1; r < n; ++r) cudaStreamSynchronize(cs[r]->stream);
+  int rc = domain_step(cs, n, t, H, counters, fail_stage);
+  if (rc)
+    for (int r = 1; r < n; ++r) cs[r]->err = cs[0]->err;
+  return rc;
+}
+
+// ---------------- host-only inspection ----------------
+int mr_coupling_inspect(const char* text, int m, int* s, int* kinds, int* eval_at, int* n_sub,
+                        char* err, size_t errlen)
+{
+  if (!text) return MR_CONTRACT;
+  Coupling cp;
+  std::string e;
+  const int rc = read_coupling_text(text, cp, e);
+  if (rc) {
+    if (err && errlen) std::snprintf(err, errlen, "%s", e.c_str());
+    return rc;
+  }
+  if (s) *s = cp.s;
+  for (int i = 0; i < cp.s; ++i) {
+    if (kinds) kinds[i] = cp.kind[i];
+    if (eval_at) eval_at[i] = cp.eval_at[i] ? 1 : 0;
+    if (n_sub) {
+      n_sub[i] = 0;
+      if (i > 0 && cp.kind[i] == MR_STAGE_FAST_IVP)
+        n_sub[i] = (int)std::max(1L, std::lround((double)m * (cp.c[i] - cp.c[i - 1])));
+    }
+  }
+  return MR_OK;
+}
+
+int mr_step_counts(const char* text, int s_f, int m, int fast_present, int slow_present,
+                   uint64_t* counters, char* err, size_t errlen)
+{
+  if (!text || !counters || s_f < 1 || m < 1) return MR_CONTRACT;
+  mr_ctx tmp;
+  std::string e;
+  const int rc = read_coupling_text(text, tmp.cp, e);
+  if (rc) {
+    if (err && errlen) std::snprintf(err, errlen, "%s", e.c_str());
+    return rc;
+  }
+  tmp.has_coupling = true;
+  tmp.tab.s = s_f;
+  tmp.m = m;
+  tmp.fast_kind = fast_present ? FK_LINEAR : FK_NONE;
+  tmp.slow_kind = slow_present ? SK_LINEAR : SK_NONE;
+  const Plan p = build_plan(&tmp);
+  for (const Op& o : p.ops)
+    if (o.type == Op::MISSING) {
+      if (err && errlen) std::snprintf(err, errlen, "missing slow value at stage %d", o.stage);
+      return MR_INTEGRATION;
+    }
+  add_counts_full(&tmp, p, 0.0, 1.0, counters);
+  return MR_OK;
+}
+
+// ---------------- instrumentation ----------------
+void* mr_stream(mr_ctx* c) { return c ? (void*)c->stream : nullptr; }
+uint64_t mr_launch_count(const mr_ctx* c) { return c ? c->launches : 0; }
+double mr_chem_flops_per_eval(const mr_ctx* c) { return c ? c->chem_flops : 0.0; }
+
+int mr_fp64_peak(mr_ctx* c, double* tflops)
+{
+  if (!c || !tflops) return MR_CONTRACT;
+  cudaSetDevice(c->device);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  double best = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(a, c->stream);
+    MR_CUDA_TRY(c, launch_fp64_peak(c->d_red, blocks, threads, iters, c->stream));
+    cudaEventRecord(b, c->stream);
+    MR_CUDA_TRY(c, cudaEventSynchronize(b));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    const double flops = 2.0 * 64.0 * (double)iters * blocks * threads;
+    if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *tflops = best;
+  return MR_OK;
+}
+
+int mr_set_graphs(mr_ctx* c, int enable)
+{
+  if (!c) return MR_CONTRACT;
+  c->graphs = enable != 0;
+  return MR_OK;
+}
+
+int mr_set_profiling(mr_ctx* c, int enable)
+{
+  if (!c) return MR_CONTRACT;
+  c->profile = enable != 0;
+  return MR_OK;
+}
+
+int mr_last_step_profile(const mr_ctx* c, double* chem_ms, double* slow_ms, double* other_ms)
+{
+  if (!c) return MR_CONTRACT;
+  if (chem_ms) *chem_ms = c->prof_chem;
+  if (slow_ms) *slow_ms = c->prof_slow;
+  if (other_ms) *other_ms = c->prof_other;
+  return MR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+"""Generate the golden fixtures of tests/golden/ with the REFERENCE's own
+stepper (oracle/_ref: /root/reference/proj/src compiled unmodified, driving
+the builder's physics callbacks through its PartitionedSystem).
+
+Run here, where /root/reference exists:  python -m tests.golden.make_golden
+The fixtures then pin the C restatement (oracle/mri_oracle.c) and the GPU
+path on the GPU box, where /root/reference does not exist.
+"""
+import json
+import os
+
+import numpy as np
+
+import oracle as O
+from paper_2211_03293_b200.configs import CONFIGS
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+# LinearTwoRateOde::default_problem (proj/src/models.cpp:65-73)
+A_FAST = np.array([[0.0, 4.0], [-4.0, 0.0]])
+A_SI = np.array([[-1.0, 0.2], [0.3, -0.7]])
+A_SE = np.array([[0.1, 0.4], [-0.3, -0.1]])
+Y0_LIN = np.array([1.0, 0.6])
+
+
+def physics_system(name, n, **kw):
+    cfg = CONFIGS[name]
+    S, R = cfg["S"], cfg["R"]
+    mech = O.mechanism(cfg["mech_seed"], S, R)
+    prof = O.velocity_profiles(cfg["vel_seed"], n, n, n) if cfg["velocity"] == "random" else None
+    sysm = O.System(n, n, n, S + 1, fast=kw.get("fast", "chem"), slow="stencil", mech=mech, S=S,
+                    R=R, rho=cfg["rho"], order=cfg["order"], diffusion=cfg["diffusion"],
+                    u=cfg["u"] or (1.0, 1.0, 1.0), prof=prof)
+    return cfg, sysm
+
+
+def main():
+    out = {}
+    meta = {}
+    couplings = {n: open(os.path.join(HERE, "couplings", f"{n}.txt")).read()
+                 for n in ["mis-kw3", "imex-mri-gark4-explicit", "imex-mri-gark3b", "imex-mri-gark4"]}
+
+    # 1. reacting-flow workloads on 8^3 with each config's physics and method
+    for name, steps in [("C1", 2), ("C2", 2), ("C3", 1), ("C4", 1)]:
+        n = 8
+        cfg, sysm = physics_system(name, n)
+        y0 = sysm.initial_condition(cfg["ic_seed"])
+        cp = couplings[cfg["coupling"]] if cfg["coupling"] != "mis-kw3" else "mis-kw3"
+        H = cfg["H"]
+        y, cnt = sysm.mri_integrate(cp, cfg["fast_table"], cfg["m"], 0.0, steps * H, H, y0,
+                                    use_reference=True)
+        out[f"{name}_n8_y"] = y
+        out[f"{name}_n8_counters"] = cnt
+        meta[f"{name}_n8"] = dict(steps=steps, H=H, n=n)
+        print(name, "counters", cnt.tolist())
+
+    # 2. reaction-off transport run with a transport-scale H (stencil visible)
+    cfg, sysm = physics_system("C3", 12, fast="none")
+    y0 = sysm.initial_condition(cfg["ic_seed"])
+    H = 2e-4
+    y, cnt = sysm.mri_integrate(couplings["imex-mri-gark4-explicit"], "classic-rk4", 4, 0.0, 3 * H,
+                                H, y0, use_reference=True)
+    out["transport_n12_y"] = y
+    out["transport_n12_counters"] = cnt
+    meta["transport_n12"] = dict(H=H, steps=3, m=4, config="C3", fast="none")
+
+    # 3. LinearTwoRateOde per cell through the reference mri_integrate
+    for cp_name, table, m in [("mis-kw3", "bogacki-shampine3", 10),
+                              ("imex-mri-gark4-explicit", "classic-rk4", 10)]:
+        spec = cp_name if cp_name == "mis-kw3" else couplings[cp_name]
+        lin = O.System(1, 1, 1, 2, fast="linear", slow="linear", fast_A=A_FAST, slow_A=A_SI + A_SE)
+        for H in (0.1, 0.05):
+            y, cnt = lin.mri_integrate(spec, table, m, 0.0, 1.0, H, Y0_LIN, use_reference=True)
+            out[f"lin_{cp_name}_{H}_y"] = y
+            out[f"lin_{cp_name}_{H}_counters"] = cnt
+    np.savez_compressed(os.path.join(HERE, "ref_fixtures.npz"), **out)
+    with open(os.path.join(HERE, "ref_fixtures.json"), "w") as f:
+        json.dump(meta, f, indent=1, sort_keys=True)
+    print("wrote", len(out), "arrays")
+
+
+if __name__ == "__main__":
+    main()
