@@ -552,39 +552,50 @@ double orc_temperature(const orc_mech* m, const double* v, size_t stride)
   return (2.0 * de) / (E1 + sqrt(E1 * E1 + 4.0 * E2 * de));
 }
 
-/* One cell of the chemistry RHS.  v/out strided by `stride` (species-major). */
+/* One cell of the chemistry RHS.  v/out strided by `stride` (species-major).
+ *   C_k  = rho Y_k / W_k,   E_k = exp(g_k/RT)
+ *   Dp_k = (E_k C_k) (RT/P),   Ei_k = (1/E_k) (P/RT)   (absent slot: 1, 1, 1)
+ *   kf_j = exp(lnA + beta lnT - Ea/(Rc T))
+ *   q_j  = kf_j (C_r1 C_r2 - (Dp_p1 Dp_p2)(Ei_r1 Ei_r2))
+ * i.e. kr = kf / Kc, Kc = exp(-dG/RT) (P/RT)^dnu: each present product
+ * contributes RT/P and each present reactant P/RT, so (RT/P)^dnu needs no
+ * per-reaction logic. */
 static void chem_cell(const orc_mech* m, const double* v, double* out, size_t stride,
-                      double* E, double* Ei, double* C, double* q)
+                      double* D, double* Ei, double* C, double* q)
 {
   const int S = m->S, R = m->R;
   const double T = orc_temperature(m, v, stride);
   const double lnT = log(T);
   const double invT = 1.0 / T;
+  const double RTP = (R_U / P_ATM) * T;
+  const double iRTP = 1.0 / RTP;
   for (int k = 0; k < S; ++k) {
     const double* sp = m->species + 5 * k;
     const double g = sp[3] * invT + sp[1] * (1.0 - lnT) - m->hb[k] * T - sp[4];
-    E[k] = exp(g);
-    Ei[k] = 1.0 / E[k];
+    const double E = exp(g);
     C[k] = m->rhoW[k] * v[(size_t)k * stride];
+    Ei[k] = (1.0 / E) * iRTP;
+    D[k] = (E * C[k]) * RTP;
   }
-  E[S] = 1.0; Ei[S] = 1.0; C[S] = 1.0; /* absent-slot dummy */
-  const double RTP = (R_U / P_ATM) * T;
-  const double iRTP = 1.0 / RTP;
+  D[S] = 1.0; Ei[S] = 1.0; C[S] = 1.0; /* absent-slot dummy */
   for (int j = 0; j < R; ++j) {
     const double* rp = m->reactions + 3 * j;
     const int* rs = m->rspecies + 4 * j;
     const int r1 = rs[0], r2 = rs[1] < 0 ? S : rs[1];
     const int p1 = rs[2], p2 = rs[3] < 0 ? S : rs[3];
     const double kf = exp(rp[0] + rp[1] * lnT - rp[2] * invT);
-    double kr = kf * E[p1] * E[p2] * Ei[r1] * Ei[r2];
-    if (m->dnu[j] == 1) kr = kr * RTP;
-    else if (m->dnu[j] == -1) kr = kr * iRTP;
-    q[j] = kf * C[r1] * C[r2] - kr * C[p1] * C[p2];
+    const double fwd = C[r1] * C[r2];
+    const double rev = (D[p1] * D[p2]) * (Ei[r1] * Ei[r2]);
+    q[j] = kf * (fwd - rev);
   }
+  /* production: w_k = sum over reactions producing k (ascending) minus the
+   * sum over reactions consuming k (ascending), accumulated in that order */
   for (int k = 0; k < S; ++k) {
     double w = 0.0;
     for (int p = m->csr_off[k]; p < m->csr_off[k + 1]; ++p)
-      w = m->csr_sgn[p] > 0 ? w + q[m->csr_rxn[p]] : w - q[m->csr_rxn[p]];
+      if (m->csr_sgn[p] > 0) w = w + q[m->csr_rxn[p]];
+    for (int p = m->csr_off[k]; p < m->csr_off[k + 1]; ++p)
+      if (m->csr_sgn[p] < 0) w = w - q[m->csr_rxn[p]];
     out[(size_t)k * stride] = m->Wrho[k] * w;
   }
   out[(size_t)S * stride] = 0.0; /* constant-volume adiabatic: de/dt = 0 */

@@ -63,6 +63,45 @@ struct ChemDev {
   double RuP;            // R_u / P_atm
 };
 
+// Mechanism for the chemistry kernel.  Scalars and per-species data travel
+// in the kernel parameter space (constant bank); the per-reaction records and
+// the production lists live in a device blob that every block stages into
+// shared memory once per launch, so the hot loops read them with broadcast
+// LDS.128 (no per-thread constant indexing, no index decoding).
+#define MR_CHEM_MAXS 64    // species + 1 (absent-reactant dummy slot)
+#define MR_CHEM_MAXR 1024
+#define MR_CHEM_MAXCHUNK 6
+struct ChemRec {           // 48 B, one per reaction
+  double lnA, beta, EaR;
+  unsigned r1o, r2o;       // byte offsets of the reactant rows in the (C, E') double2 table
+  unsigned p1o, p2o;       // byte offsets of the product rows in the D' table
+  unsigned pad0, pad1;
+};
+struct ChemParams {
+  int S, R;
+  int rc, nchunk;          // reactions per rate-buffer chunk, number of chunks
+  double RuP;
+  const uint4* blob;       // [R ChemRec][production entries], 16-B aligned
+  int blob_words;          // size of the blob in uint4
+  int ent_base;            // first entry word (uint4 index) of the production lists
+  double h0[MR_CHEM_MAXS], a[MR_CHEM_MAXS], hb[MR_CHEM_MAXS], s0[MR_CHEM_MAXS];
+  double rhoW[MR_CHEM_MAXS], Wrho[MR_CHEM_MAXS];
+  double c0[MR_CHEM_MAXS], c1[MR_CHEM_MAXS], c2[MR_CHEM_MAXS];
+  // species k, chunk ch: {plus start, plus count, minus start, minus count}
+  // in uint4 words relative to ent_base; entries are byte offsets of q rows
+  // (chunk-local), lists padded to 4 with the offset of an all-zero row
+  ushort4 lst[MR_CHEM_MAXS][MR_CHEM_MAXCHUNK];
+  // slot (w + NW*t) -> component owned by that thread; >= ncomp = idle.
+  // Greedy-balanced on the species' production-list lengths.
+  unsigned char perm[MR_CHEM_MAXS];
+};
+
+struct ChemCfg {
+  int NW, SPL;  // warps per block (slots), components per thread
+  bool subdiag;
+  int ndeg;
+};
+
 struct LinDev {
   int n;
   double A[MR_MAXLIN * MR_MAXLIN];
@@ -113,6 +152,14 @@ cudaError_t launch_chain(const ChainCfg& cfg, const ChainArgs& a, const ChemDev&
 cudaError_t launch_fast_rhs(const ChainCfg& cfg, const double* y, double* out, size_t ncell,
                             int ncomp, const ChemDev& ch, const LinDev& lin, cudaStream_t st);
 size_t chain_smem_bytes(const ChainCfg& cfg, int S, int R, int block);
+
+int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int ndeg);
+int chem_chunking(int NW, int S, int R, size_t blob_bytes, int* rc, int* nchunk);
+cudaError_t launch_chem_chain(const ChemCfg& cfg, const ChainArgs& a, const ChemParams& P,
+                              cudaStream_t st);
+cudaError_t launch_chem_rhs(const ChemCfg& cfg, const double* y, double* out, size_t ncell,
+                            int ncomp, const ChemParams& P, cudaStream_t st);
+size_t chem_smem_bytes(const ChemCfg& cfg, int S, int R);
 
 cudaError_t launch_update(const double* y_in, double* y_out, int nref, const double* const* f,
                           const double* coef, size_t n, int mri_stage,

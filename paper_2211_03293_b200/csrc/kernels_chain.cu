@@ -25,6 +25,9 @@
 // CSR orders, so results are bitwise run-to-run deterministic.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace {
@@ -408,6 +411,17 @@ int chain_pick(ChainCfg* cfg, int fast_kind, int ncomp, int S, int R, int s_f, i
   else if (ncomp <= 32) { cfg->G = 16; cfg->SPL = 2; }
   else if (ncomp <= 64) { cfg->G = 32; cfg->SPL = 2; }
   else return 1;
+  // experiment hook: MR_CHEM_LAYOUT="G,SPL" forces an instantiated layout
+  if (const char* env = getenv("MR_CHEM_LAYOUT")) {
+    int g = 0, spl = 0;
+    if (sscanf(env, "%d,%d", &g, &spl) == 2 && g * spl >= ncomp) {
+      bool known = false;
+#define MR_KNOWN(GG, SS) known |= (g == GG && spl == SS);
+      MR_CHEM_LAYOUTS(MR_KNOWN)
+#undef MR_KNOWN
+      if (known) { cfg->G = g; cfg->SPL = spl; }
+    }
+  }
   return 0;
 }
 
@@ -431,8 +445,7 @@ cudaError_t launch_chain(const ChainCfg& cfg, const ChainArgs& a, const ChemDev&
   if (cfg.G == GG && cfg.SPL == SS) { MR_DISPATCH_MS(FK_CHEM, GG, SS) }
 #define MR_NONE_CASE(GG, SS) \
   if (cfg.G == GG && cfg.SPL == SS) { MR_DISPATCH_MS(FK_NONE, GG, SS) }
-  if (cfg.fast_kind == FK_CHEM) { MR_CHEM_LAYOUTS(MR_CHEM_CASE) }
-  else if (cfg.fast_kind == FK_NONE) { MR_CHEM_LAYOUTS(MR_NONE_CASE) }
+  if (cfg.fast_kind == FK_NONE) { MR_CHEM_LAYOUTS(MR_NONE_CASE) }
   else if (cfg.fast_kind == FK_LINEAR) {
     if (cfg.SPL == 2) { MR_DISPATCH_MS(FK_LINEAR, 1, 2) }
     if (cfg.SPL == 4) { MR_DISPATCH_MS(FK_LINEAR, 1, 4) }
@@ -449,8 +462,7 @@ cudaError_t launch_fast_rhs(const ChainCfg& cfg, const double* y, double* out, s
   if (cfg.G == GG && cfg.SPL == SS) return run_rhs<FK_CHEM, GG, SS>(y, out, ncell, ncomp, ch, lin, smem, st);
 #define MR_RHS_NONE(GG, SS) \
   if (cfg.G == GG && cfg.SPL == SS) return run_rhs<FK_NONE, GG, SS>(y, out, ncell, ncomp, ch, lin, smem, st);
-  if (cfg.fast_kind == FK_CHEM) { MR_CHEM_LAYOUTS(MR_RHS_CHEM) }
-  else if (cfg.fast_kind == FK_NONE) { MR_CHEM_LAYOUTS(MR_RHS_NONE) }
+  if (cfg.fast_kind == FK_NONE) { MR_CHEM_LAYOUTS(MR_RHS_NONE) }
   else if (cfg.fast_kind == FK_LINEAR) {
     if (cfg.SPL == 2) return run_rhs<FK_LINEAR, 1, 2>(y, out, ncell, ncomp, ch, lin, smem, st);
     if (cfg.SPL == 4) return run_rhs<FK_LINEAR, 1, 4>(y, out, ncell, ncomp, ch, lin, smem, st);

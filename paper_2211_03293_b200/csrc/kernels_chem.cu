@@ -1,0 +1,103 @@
+// kernels_chem.cu -- host side of K1 for the chemistry plugin: layout
+// choice, rate-buffer chunking and dispatch to the per-layout instantiations
+// (kernels_chem_nw*.cu).  Kernel design: kernels_chem.cuh.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "kernels_chem.cuh"
+
+namespace mrchem {
+#define MR_DECL(A, B)                                                                      \
+  extern template cudaError_t run_chem_chain<A, B, true, 4, 1>(const ChainArgs&, const ChemParams&, cudaStream_t);  \
+  extern template cudaError_t run_chem_chain<A, B, true, 4, 2>(const ChainArgs&, const ChemParams&, cudaStream_t);  \
+  extern template cudaError_t run_chem_chain<A, B, false, 6, 1>(const ChainArgs&, const ChemParams&, cudaStream_t); \
+  extern template cudaError_t run_chem_chain<A, B, false, 6, 2>(const ChainArgs&, const ChemParams&, cudaStream_t); \
+  extern template cudaError_t run_chem_rhs<A, B>(const double*, double*, size_t, int, const ChemParams&, cudaStream_t);
+MR_DECL(4, 3)
+MR_DECL(8, 3)
+MR_DECL(8, 7)
+MR_DECL(16, 4)
+#undef MR_DECL
+}  // namespace mrchem
+
+// (NW warps = slots, SPL components per thread) layouts
+#define MR_CHEM_BLOCK_LAYOUTS(X) X(4, 3) X(8, 3) X(8, 7) X(16, 4)
+
+int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int ndeg)
+{
+  (void)R;
+  if (S + 1 > MR_CHEM_MAXS || ndeg < 1 || ndeg > MR_MAXDEG || tab.s > MR_MAXS) return 1;
+  bool subdiag = true;
+  for (int i = 0; i < tab.s; ++i)
+    for (int j = 0; j < i - 1; ++j)
+      if (tab.A[i][j] != 0.0) subdiag = false;
+  cfg->subdiag = subdiag;
+  cfg->ndeg = ndeg;
+  if (ncomp <= 12) { cfg->NW = 4; cfg->SPL = 3; }
+  else if (ncomp <= 24) { cfg->NW = 8; cfg->SPL = 3; }
+  else if (ncomp <= 64) { cfg->NW = 16; cfg->SPL = 4; }
+  else return 1;
+  if (const char* env = getenv("MR_CHEM_BLOCK")) {  // experiment hook "NW,SPL"
+    int nw = 0, spl = 0;
+    if (sscanf(env, "%d,%d", &nw, &spl) == 2 && nw * spl >= ncomp) {
+      bool known = false;
+#define MR_KNOWN(A, B) known |= (nw == A && spl == B);
+      MR_CHEM_BLOCK_LAYOUTS(MR_KNOWN)
+#undef MR_KNOWN
+      if (known) { cfg->NW = nw; cfg->SPL = spl; }
+    }
+  }
+  return 0;
+}
+
+// rate-buffer chunking: largest chunk (multiple of NW) such that two blocks
+// fit the 227 KB shared memory of an SM (one block for NW = 16)
+int chem_chunking(int NW, int S, int R, size_t blob_bytes, int* rc, int* nchunk)
+{
+  const size_t budget = (size_t)(NW <= 8 ? 113 : 227) * 1024;
+  const size_t fixed = mrchem::smem_bytes(NW, S + 1, 0, (int)((blob_bytes + 15) / 16));
+  if (fixed >= budget) return 1;
+  int cap = (int)((budget - fixed) / 256);
+  cap -= cap % NW;
+  if (cap < NW) return 1;
+  int n = (R + cap - 1) / cap;
+  if (n > MR_CHEM_MAXCHUNK) return 1;
+  int size = (R + n - 1) / n;
+  size = (size + NW - 1) / NW * NW;
+  *rc = size;
+  *nchunk = n;
+  return 0;
+}
+
+cudaError_t launch_chem_chain(const ChemCfg& cfg, const ChainArgs& a, const ChemParams& P,
+                              cudaStream_t st)
+{
+#define MR_CHEM_DISPATCH(A, B)                                                              \
+  if (cfg.NW == A && cfg.SPL == B) {                                                        \
+    if (cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem_chain<A, B, true, 4, 1>(a, P, st);   \
+    if (cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem_chain<A, B, true, 4, 2>(a, P, st);   \
+    if (!cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem_chain<A, B, false, 6, 1>(a, P, st); \
+    if (!cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem_chain<A, B, false, 6, 2>(a, P, st); \
+  }
+  MR_CHEM_BLOCK_LAYOUTS(MR_CHEM_DISPATCH)
+#undef MR_CHEM_DISPATCH
+  return cudaErrorInvalidConfiguration;
+}
+
+cudaError_t launch_chem_rhs(const ChemCfg& cfg, const double* y, double* out, size_t ncell,
+                            int ncomp, const ChemParams& P, cudaStream_t st)
+{
+#define MR_CHEM_RHS(A, B) \
+  if (cfg.NW == A && cfg.SPL == B) return mrchem::run_chem_rhs<A, B>(y, out, ncell, ncomp, P, st);
+  MR_CHEM_BLOCK_LAYOUTS(MR_CHEM_RHS)
+#undef MR_CHEM_RHS
+  return cudaErrorInvalidConfiguration;
+}
+
+size_t chem_smem_bytes(const ChemCfg& cfg, int S, int R)
+{
+  (void)R;
+  return mrchem::smem_bytes(cfg.NW, S + 1, 0, 0);
+}

@@ -1,0 +1,472 @@
+// kernels_chem.cuh -- K1 for the chemistry plugin: the fused fast-IVP
+// kernel with the per-cell Arrhenius RHS (templates; instantiated per layout
+// in kernels_chem_nw*.cu so the variants compile in parallel).
+//
+// Stage semantics are those of kernels_chain.cu -- build_forcing, n_sub
+// erk_step substeps, the fast_rhs lambda, explicit updates and the all_finite
+// checks (proj/src/mri.cpp:354-433, proj/src/erk.cpp:9-38) -- with the RHS
+// organised for the GPU:
+//
+//   * a block owns 32 cells (lane = cell) and NW warps.  Warp w owns the
+//     components k = w + NW*t of all 32 cells (the RK state stays in
+//     registers), the reactions j = w, w+NW, ... and, in the production
+//     phase, its own species.  Every mechanism index is therefore identical
+//     across the 32 lanes: constant-bank reads are broadcasts and every
+//     shared-memory access is one [item][32 cells] row -- 256 B (or 512 B
+//     for the double2 reactant rows), no bank conflicts, no divergence;
+//   * (RT/P)^dnu is folded into the per-species rows (each present product
+//     contributes RT/P, each present reactant P/RT), so a reaction is
+//     branch-free: kf = exp(lnA + beta lnT - Ea/RcT),
+//     q = kf (C_r1 C_r2 - (D'_p1 D'_p2)(E'_r1 E'_r2));
+//   * mechanism topology is pre-baked into shared-memory byte offsets
+//     (ChemParams::roff/poff/csr_ent), so there is no index decoding;
+//   * rates of progress pass through a chunked shared buffer and are gathered
+//     per species in a fixed order (reaction ascending): bitwise deterministic
+//     and the oracle's summation order;
+//   * exp is a branch-free degree-13 reduction + Horner with its coefficients
+//     in the constant bank (~1 ulp; overflow -> inf, NaN stays NaN).
+//
+// Per RHS evaluation and cell: shared traffic 48 B gathered + 8 B stored per
+// reaction + 8 B per species-reaction incidence; fp64 work ~25 ops per
+// reaction.  Two blocks per SM overlap each other's barriers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace mrchem {
+
+#ifndef MR_CHEM_PERM
+#define MR_KK(slot) (slot)
+#else
+#define MR_KK(slot) (P.perm[slot])
+#endif
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+static __constant__ double kExpC[16] = {
+    1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0,
+    1.0 / 40320.0,      1.0 / 5040.0,      1.0 / 720.0,      1.0 / 120.0,     1.0 / 24.0,
+    1.0 / 6.0,          0.5,               1.0,              1.0,             1.4426950408889634,
+    -6.93147180559890330187e-01};
+
+// exp(x) = 2^n e^r, |r| <= ln2/2, Taylor degree 13 by Horner (~1 ulp).  An
+// Estrin form (depth 4) measured 12% slower here: its 11 live doubles per
+// exp cost more occupancy than the shorter dependency chain gains.
+__device__ __forceinline__ double mr_exp(double x)
+{
+  const double t = fma(x, kExpC[14], 6755399441055744.0);
+  const double nd = t - 6755399441055744.0;
+  const int n = min(max(__double2loint(t), -1022), 1024);
+  double r = fma(nd, kExpC[15], x);
+  r = fma(nd, -5.49792301870837115524e-14, r);
+  double p = kExpC[0];
+#pragma unroll
+  for (int i = 1; i < 14; ++i) p = fma(p, r, kExpC[i]);
+  return p * __hiloint2double((n + 1023) << 20, 0);
+}
+
+// shared memory (bytes are what the offset tables index)
+//   CE   double2 [S1][32]   (C_k, (P/RT)/E_k)          row = 512 B
+//   D    double  [S1][32]   E_k C_k RT/P                row = 256 B
+//   q    double  [rc][32]   rates of progress (chunk)   row = 256 B
+//   zero double  [32]       padding target of the production lists
+//   blob uint4   [words]    ChemRec[R] + production lists (staged per launch)
+//   part double  [4][NW][32]
+//   tinf double  [3][32]    T, lnT, 1/T
+__host__ __device__ inline size_t smem_bytes(int NW, int S1, int rc, int blob_words)
+{
+  return (size_t)S1 * 512 + (size_t)S1 * 256 + (size_t)rc * 256 + 256 + (size_t)blob_words * 16 +
+         (size_t)4 * NW * 256 + 3 * 256;
+}
+
+struct Smem {
+  char* CE;
+  char* D;
+  char* q;
+  const char* rec;
+  const uint4* ent;
+  double* part;
+  double* tinf;
+};
+
+// carves shared memory and stages the mechanism blob (all threads; ends with
+// a barrier)
+__device__ __forceinline__ Smem stage(char* base, const ChemParams& P, int NW, int c, int w)
+{
+  const int S1 = P.S + 1;
+  Smem m;
+  m.CE = base;
+  m.D = m.CE + S1 * 512;
+  m.q = m.D + S1 * 256;
+  char* zero = m.q + P.rc * 256;
+  uint4* blob = reinterpret_cast<uint4*>(zero + 256);
+  m.rec = reinterpret_cast<const char*>(blob);
+  m.ent = blob + P.ent_base;
+  m.part = reinterpret_cast<double*>(blob + P.blob_words);
+  m.tinf = m.part + 4 * NW * 32;
+  for (int i = threadIdx.x; i < P.blob_words; i += blockDim.x) blob[i] = __ldg(P.blob + i);
+  if (w == 0) {
+    reinterpret_cast<double*>(zero)[c] = 0.0;
+    // absent-species dummy rows: C = E' = D' = 1
+    *reinterpret_cast<double2*>(m.CE + P.S * 512 + c * 16) = make_double2(1.0, 1.0);
+    *reinterpret_cast<double*>(m.D + P.S * 256 + c * 8) = 1.0;
+  }
+  __syncthreads();
+  return m;
+}
+
+template <class T>
+__device__ __forceinline__ const T& at(const char* base, unsigned off)
+{
+  return *reinterpret_cast<const T*>(base + off);
+}
+
+// One chemistry RHS evaluation for the block's 32 cells (all threads call it).
+template <int NW, int SPL>
+__device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem& m, int w, int c,
+                                                const int (&kk)[SPL], const double (&v)[SPL],
+                                                double (&f)[SPL])
+{
+  const int S = P.S;
+  const unsigned lane8 = (unsigned)c * 8u, lane16 = (unsigned)c * 16u;
+  // ---- temperature from energy: partial sums of e(T) = E0 + E1 T + E2 T^2
+  {
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, e = 0.0;
+#pragma unroll
+    for (int t = 0; t < SPL; ++t) {
+      const int k = kk[t];
+      if (k < S) {
+        p0 += v[t] * P.c0[k];
+        p1 += v[t] * P.c1[k];
+        p2 += v[t] * P.c2[k];
+      } else if (k == S) {
+        e = v[t];
+      }
+    }
+    m.part[(0 * NW + w) * 32 + c] = p0;
+    m.part[(1 * NW + w) * 32 + c] = p1;
+    m.part[(2 * NW + w) * 32 + c] = p2;
+    m.part[(3 * NW + w) * 32 + c] = e;
+  }
+  __syncthreads();
+  if (w == 0) {
+    double E0 = 0.0, E1 = 0.0, E2 = 0.0, ee = 0.0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+      E0 += m.part[(0 * NW + q) * 32 + c];
+      E1 += m.part[(1 * NW + q) * 32 + c];
+      E2 += m.part[(2 * NW + q) * 32 + c];
+      ee += m.part[(3 * NW + q) * 32 + c];
+    }
+    const double de = ee - E0;
+    const double T = (2.0 * de) / (E1 + sqrt(E1 * E1 + 4.0 * E2 * de));
+    m.tinf[0 * 32 + c] = T;
+    m.tinf[1 * 32 + c] = log(T);
+    m.tinf[2 * 32 + c] = 1.0 / T;
+  }
+  __syncthreads();
+  const double T = m.tinf[0 * 32 + c];
+  const double lnT = m.tinf[1 * 32 + c];
+  const double invT = m.tinf[2 * 32 + c];
+
+  // ---- species rows: (C_k, (1/E_k)(P/RT)) and (E_k C_k)(RT/P)
+  {
+    const double RTP = P.RuP * T;
+    const double iRTP = 1.0 / RTP;
+#pragma unroll
+    for (int t = 0; t < SPL; ++t) {
+      const int k = kk[t];
+      if (k < S) {
+        const double g = P.h0[k] * invT + P.a[k] * (1.0 - lnT) - P.hb[k] * T - P.s0[k];
+        const double E = mr_exp(g);
+        const double Ck = P.rhoW[k] * v[t];
+        *reinterpret_cast<double2*>(m.CE + k * 512 + lane16) = make_double2(Ck, (1.0 / E) * iRTP);
+        *reinterpret_cast<double*>(m.D + k * 256 + lane8) = (E * Ck) * RTP;
+      }
+    }
+  }
+  __syncthreads();
+
+  double acc[SPL];
+#pragma unroll
+  for (int t = 0; t < SPL; ++t) acc[t] = 0.0;
+  const int R = P.R;
+  const char* CEl = m.CE + lane16;
+  const char* Dl = m.D + lane8;
+  const char* ql = m.q + lane8;
+  for (int ch = 0; ch < P.nchunk; ++ch) {
+    const int j0 = ch * P.rc;
+    const int j1 = min(R, j0 + P.rc);
+    // ---- reactions of this chunk:
+    //      q = kf (C_r1 C_r2 - (D'_p1 D'_p2)(E'_r1 E'_r2)), kf = exp(lnA + beta lnT - EaR/T)
+    char* qw = m.q + lane8 + (unsigned)w * 256u;
+    const char* rp = m.rec + (j0 + w) * (int)sizeof(ChemRec);
+#pragma unroll 2
+    for (int j = j0 + w; j < j1; j += NW) {
+      const double2 ab = *reinterpret_cast<const double2*>(rp);
+      const uint4 er = *reinterpret_cast<const uint4*>(rp + 16);
+      const uint2 pp = *reinterpret_cast<const uint2*>(rp + 32);
+      const double EaR = __hiloint2double((int)er.y, (int)er.x);
+      const double kf = mr_exp(fma(-EaR, invT, fma(ab.y, lnT, ab.x)));
+      const double2 a1 = at<double2>(CEl, er.z);
+      const double2 a2 = at<double2>(CEl, er.w);
+      const double d1 = at<double>(Dl, pp.x);
+      const double d2 = at<double>(Dl, pp.y);
+      const double fwd = a1.x * a2.x;
+      const double rev = (d1 * d2) * (a1.y * a2.y);
+      *reinterpret_cast<double*>(qw) = kf * (fwd - rev);
+      qw += NW * 256;
+      rp += NW * (int)sizeof(ChemRec);
+    }
+    __syncthreads();
+    // ---- production: w_k += sum_(producing) q - sum_(consuming) q, reaction
+    //      ascending, four entries per broadcast LDS.128 (padding -> zero row)
+#pragma unroll
+    for (int t = 0; t < SPL; ++t) {
+      const int k = kk[t];
+      if (k < S) {
+        const ushort4 L = P.lst[k][ch];
+        double s_ = acc[t];
+        for (int i = 0; i < L.y; ++i) {
+          const uint4 e = m.ent[L.x + i];
+          s_ += at<double>(ql, e.x);
+          s_ += at<double>(ql, e.y);
+          s_ += at<double>(ql, e.z);
+          s_ += at<double>(ql, e.w);
+        }
+        for (int i = 0; i < L.w; ++i) {
+          const uint4 e = m.ent[L.z + i];
+          s_ -= at<double>(ql, e.x);
+          s_ -= at<double>(ql, e.y);
+          s_ -= at<double>(ql, e.z);
+          s_ -= at<double>(ql, e.w);
+        }
+        acc[t] = s_;
+      }
+    }
+    if (ch + 1 < P.nchunk) __syncthreads();  // q is overwritten by the next chunk
+  }
+#pragma unroll
+  for (int t = 0; t < SPL; ++t) {
+    const int k = kk[t];
+    f[t] = k < S ? P.Wrho[k] * acc[t] : 0.0;  // energy: de/dt = 0
+  }
+}
+
+template <int NW, int SPL, bool SUBDIAG, int MAXS, int NDEG>
+__global__ void __launch_bounds__(NW * 32, (NW <= 8 ? 2 : 1))
+    chem_chain_kernel(const __grid_constant__ ChainArgs a, const __grid_constant__ ChemParams P)
+{
+  extern __shared__ __align__(16) double smem_raw[];
+  const int c = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const size_t cell = (size_t)blockIdx.x * 32 + c;
+  const bool active = cell < a.ncell;
+  const size_t nc = a.ncell;
+  const int ncomp = a.ncomp;
+  const Smem m = stage(reinterpret_cast<char*>(smem_raw), P, NW, c, w);
+  int kk[SPL];  // components owned by this thread (load-balanced permutation)
+#pragma unroll
+  for (int t = 0; t < SPL; ++t) kk[t] = MR_KK(w + NW * t);
+
+  double y[SPL];
+#pragma unroll
+  for (int t = 0; t < SPL; ++t) {
+    const int k = kk[t];
+    y[t] = (active && k < ncomp) ? a.y_in[(size_t)k * nc + cell] : 0.0;
+  }
+  bool failed = !active;
+
+  for (int si = 0; si < a.nst; ++si) {
+    const ChainStageDev& st = a.st[si];
+    if (st.kind != 0) {  // ExplicitUpdate: Y += sum_j (H wbar_ij) fE_j
+      for (int r = 0; r < st.nref; ++r) {
+        const double cf = st.coef[0][r];
+        if (cf == 0.0) continue;
+        const double* __restrict__ fv = a.fE[st.ref_slot[r]];
+#pragma unroll
+        for (int t = 0; t < SPL; ++t) {
+          const int k = kk[t];
+          if (active && k < ncomp) y[t] = dadd(y[t], dmul(cf, fv[(size_t)k * nc + cell]));
+        }
+      }
+      if (!failed) {
+        bool bad = false;
+#pragma unroll
+        for (int t = 0; t < SPL; ++t)
+          if (kk[t] < ncomp && !isfinite(y[t])) bad = true;
+        if (bad) {
+          atomicMin(a.fail, mr_fail_key(st.mri_stage, 0, 0));
+          failed = true;
+        }
+      }
+      continue;
+    }
+
+    // FastIvp: forcing coefficients r_k = sum_j (omega[k][i][j]/dc) fE_j
+    double rc[NDEG][SPL];
+#pragma unroll
+    for (int k = 0; k < NDEG; ++k)
+#pragma unroll
+      for (int t = 0; t < SPL; ++t) rc[k][t] = 0.0;
+    for (int r = 0; r < st.nref; ++r) {
+      const double* __restrict__ fv = a.fE[st.ref_slot[r]];
+#pragma unroll
+      for (int t = 0; t < SPL; ++t) {
+        const int kc = kk[t];
+        const double x = (active && kc < ncomp) ? fv[(size_t)kc * nc + cell] : 0.0;
+#pragma unroll
+        for (int k = 0; k < NDEG; ++k) {
+          const double cf = st.coef[k][r];
+          if (cf != 0.0) rc[k][t] = dadd(rc[k][t], dmul(cf, x));
+        }
+      }
+    }
+
+    const double h = st.h_sub;
+    const int sf = a.tab.s;
+    for (int sub = 0; sub < st.n_sub; ++sub) {
+      const double t0 = dadd(st.t_start, dmul((double)sub, h));
+      constexpr int NPRE = SUBDIAG ? 1 : MAXS;
+      double pre[NPRE][SPL];
+      double out[SPL];
+#pragma unroll
+      for (int i = 0; i < NPRE; ++i)
+#pragma unroll
+        for (int t = 0; t < SPL; ++t) pre[i][t] = y[t];
+#pragma unroll
+      for (int t = 0; t < SPL; ++t) out[t] = y[t];
+
+      for (int j = 0; j < sf; ++j) {
+        double stg[SPL];
+#pragma unroll
+        for (int t = 0; t < SPL; ++t) stg[t] = pre[0][t];
+        if constexpr (!SUBDIAG) {
+#pragma unroll
+          for (int i = 1; i < NPRE; ++i)
+            if (i == j) {
+#pragma unroll
+              for (int t = 0; t < SPL; ++t) stg[t] = pre[i][t];
+            }
+        }
+        if (!failed) {
+          bool bad = false;
+#pragma unroll
+          for (int t = 0; t < SPL; ++t)
+            if (kk[t] < ncomp && !isfinite(stg[t])) bad = true;
+          if (bad) {
+            atomicMin(a.fail, mr_fail_key(st.mri_stage, sub, j));
+            failed = true;
+          }
+        }
+        const double theta = dadd(t0, dmul(a.tab.c[j], h));
+        const double tau = __ddiv_rn(dadd(theta, -st.t_start), st.span);
+        double f[SPL];
+        chem_block_eval<NW, SPL>(P, m, w, c, kk, stg, f);
+        const double hb = dmul(h, a.tab.b[j]);
+        const bool use_b = a.tab.b[j] != 0.0;
+        double hA_next = 0.0;
+        bool useA = false;
+        if constexpr (SUBDIAG) {
+          useA = j + 1 < sf && a.tab.A[j + 1][j] != 0.0;
+          if (useA) hA_next = dmul(h, a.tab.A[j + 1][j]);
+        }
+#pragma unroll
+        for (int t = 0; t < SPL; ++t) {
+          double fr = rc[NDEG - 1][t];
+#pragma unroll
+          for (int k = NDEG - 2; k >= 0; --k) fr = dadd(dmul(fr, tau), rc[k][t]);
+          const double kj = dadd(f[t], fr);
+          if constexpr (SUBDIAG) {
+            // stage_{j+1} = y + (h A[j+1][j]) k_j, the only nonzero entry
+            if (j + 1 < sf) pre[0][t] = useA ? dadd(y[t], dmul(hA_next, kj)) : y[t];
+          } else {
+#pragma unroll
+            for (int i = 1; i < NPRE; ++i) {
+              if (i > j && i < sf) {
+                const double Aij = a.tab.A[i][j];
+                if (Aij != 0.0) pre[i][t] = dadd(pre[i][t], dmul(dmul(h, Aij), kj));
+              }
+            }
+          }
+          if (use_b) out[t] = dadd(out[t], dmul(hb, kj));
+        }
+      }
+      if (!failed) {
+        bool bad = false;
+#pragma unroll
+        for (int t = 0; t < SPL; ++t)
+          if (kk[t] < ncomp && !isfinite(out[t])) bad = true;
+        if (bad) {
+          atomicMin(a.fail, mr_fail_key(st.mri_stage, sub, sf));
+          failed = true;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < SPL; ++t) y[t] = out[t];
+    }
+  }
+
+#pragma unroll
+  for (int t = 0; t < SPL; ++t) {
+    const int k = kk[t];
+    if (active && k < ncomp) a.y_out[(size_t)k * nc + cell] = y[t];
+  }
+}
+
+template <int NW, int SPL>
+__global__ void __launch_bounds__(NW * 32) chem_rhs_kernel(const double* __restrict__ yin,
+                                                           double* __restrict__ fout, size_t nc,
+                                                           int ncomp,
+                                                           const __grid_constant__ ChemParams P)
+{
+  extern __shared__ __align__(16) double smem_raw[];
+  const int c = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const size_t cell = (size_t)blockIdx.x * 32 + c;
+  const bool active = cell < nc;
+  const Smem m = stage(reinterpret_cast<char*>(smem_raw), P, NW, c, w);
+  int kk[SPL];  // components owned by this thread (load-balanced permutation)
+#pragma unroll
+  for (int t = 0; t < SPL; ++t) kk[t] = MR_KK(w + NW * t);
+  double v[SPL], f[SPL];
+#pragma unroll
+  for (int t = 0; t < SPL; ++t) {
+    const int k = kk[t];
+    v[t] = (active && k < ncomp) ? yin[(size_t)k * nc + cell] : 0.0;
+  }
+  chem_block_eval<NW, SPL>(P, m, w, c, kk, v, f);
+#pragma unroll
+  for (int t = 0; t < SPL; ++t) {
+    const int k = kk[t];
+    if (active && k < ncomp) fout[(size_t)k * nc + cell] = f[t];
+  }
+}
+
+template <int NW, int SPL, bool SUBDIAG, int MAXS, int NDEG>
+cudaError_t run_chem_chain(const ChainArgs& a, const ChemParams& P, cudaStream_t st)
+{
+  const size_t smem = smem_bytes(NW, P.S + 1, P.rc, P.blob_words);
+  auto k = chem_chain_kernel<NW, SPL, SUBDIAG, MAXS, NDEG>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const size_t blocks = (a.ncell + 31) / 32;
+  k<<<(unsigned)blocks, NW * 32, smem, st>>>(a, P);
+  return cudaGetLastError();
+}
+
+template <int NW, int SPL>
+cudaError_t run_chem_rhs(const double* y, double* out, size_t nc, int ncomp, const ChemParams& P,
+                         cudaStream_t st)
+{
+  const size_t smem = smem_bytes(NW, P.S + 1, P.rc, P.blob_words);
+  auto k = chem_rhs_kernel<NW, SPL>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<(unsigned)((nc + 31) / 32), NW * 32, smem, st>>>(y, out, nc, ncomp, P);
+  return cudaGetLastError();
+}
+
+}  // namespace mrchem

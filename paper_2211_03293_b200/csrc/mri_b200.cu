@@ -13,7 +13,7 @@
 // Counters follow the reference's increment rules exactly (mri.cpp:342, :347,
 // :378; erk.cpp:28), including partial counts on an IntegrationError.
 #include <cuda_runtime.h>
-#include <nccl.h>
+#include "nccl_shim.h"
 
 #include <algorithm>
 #include <cmath>
@@ -168,6 +168,7 @@ struct mr_ctx {
   int S = 0, R = 0;
   double rho = 0.0;
   ChemDev chem{};
+  ChemParams* chemP = nullptr;  // host copy, passed by value to the kernels
   double chem_flops = 0.0;
   std::vector<void*> chem_bufs;
   LinDev fastA{}, slowA{};
@@ -218,9 +219,10 @@ int set_err(mr_ctx* c, int code, const std::string& msg)
 
 #define MR_NCCL_TRY(ctx, call)                                                            \
   do {                                                                                     \
-    ncclResult_t r_ = (call);                                                              \
+    if (!nccl_api().ok) return set_err(ctx, MR_CUDA, "NCCL (libnccl.so.2) not available");  \
+    ncclResult_t r_ = (nccl_api().call);                                                   \
     if (r_ != ncclSuccess)                                                                 \
-      return set_err(ctx, MR_CUDA, std::string(#call) + ": " + ncclGetErrorString(r_));    \
+      return set_err(ctx, MR_CUDA, std::string(#call) + ": " + nccl_api().GetErrorString(r_)); \
   } while (0)
 
 void free_dev(void*& p)
@@ -473,12 +475,12 @@ int exchange_halos(mr_ctx** cs, int n, const double* const* ycur, const double**
     mr_ctx* c = cs[0];
     const int left = (c->rank - 1 + c->nranks) % c->nranks;
     const int right = (c->rank + 1) % c->nranks;
-    MR_NCCL_TRY(c, ncclGroupStart());
-    MR_NCCL_TRY(c, ncclSend(c->send_lo, c->halo_elems, ncclDouble, left, c->comm, st));
-    MR_NCCL_TRY(c, ncclRecv(c->recv_hi, c->halo_elems, ncclDouble, right, c->comm, st));
-    MR_NCCL_TRY(c, ncclSend(c->send_hi, c->halo_elems, ncclDouble, right, c->comm, st));
-    MR_NCCL_TRY(c, ncclRecv(c->recv_lo, c->halo_elems, ncclDouble, left, c->comm, st));
-    MR_NCCL_TRY(c, ncclGroupEnd());
+    MR_NCCL_TRY(c, GroupStart());
+    MR_NCCL_TRY(c, Send(c->send_lo, c->halo_elems, ncclDouble, left, c->comm, st));
+    MR_NCCL_TRY(c, Recv(c->recv_hi, c->halo_elems, ncclDouble, right, c->comm, st));
+    MR_NCCL_TRY(c, Send(c->send_hi, c->halo_elems, ncclDouble, right, c->comm, st));
+    MR_NCCL_TRY(c, Recv(c->recv_lo, c->halo_elems, ncclDouble, left, c->comm, st));
+    MR_NCCL_TRY(c, GroupEnd());
     lo[0] = c->recv_lo;
     hi[0] = c->recv_hi;
     return MR_OK;
@@ -622,15 +624,19 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
   }
   cudaStream_t st = c0->stream;
   ChainCfg cfg;
-  if (chain_pick(&cfg, c0->fast_kind, c0->ncomp, c0->S, c0->R, c0->tab.s, ndeg_of(c0)))
+  ChemCfg ccfg;
+  if (c0->fast_kind == FK_CHEM) {
+    if (chem_pick(&ccfg, c0->ncomp, c0->S, c0->R, c0->tab, ndeg_of(c0)))
+      return set_err(c0, MR_CONTRACT, "unsupported mechanism size / table for the chemistry kernel");
+  } else if (chain_pick(&cfg, c0->fast_kind, c0->ncomp, c0->S, c0->R, c0->tab.s, ndeg_of(c0))) {
     return set_err(c0, MR_CONTRACT, "unsupported component count / table for the fused IVP kernel");
+  }
   for (int r = 0; r < n; ++r)
     MR_CUDA_TRY(cs[r], cudaMemsetAsync(cs[r]->d_fail, 0xFF, sizeof(unsigned long long), st));
 
   std::vector<const double*> ycur(n);
   std::vector<double*> outs(n);
   for (int r = 0; r < n; ++r) ycur[r] = cs[r]->y_state;
-  bool on_work = false;
   size_t ev = 0;
   std::vector<std::pair<int, size_t>> timed;  // (class, event index)
   int missing_stage = -1;
@@ -663,7 +669,6 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
         c->launches++;
         ycur[r] = c->y_work;
       }
-      on_work = true;
     } else {  // CHAIN
       for (int r = 0; r < n; ++r) {
         mr_ctx* c = cs[r];
@@ -679,20 +684,21 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
         a.ncell = c->ncell;
         a.ncomp = c->ncomp;
         a.fail = c->d_fail;
-        MR_CUDA_TRY(c, launch_chain(cfg, a, c->chem, c->fastA, st));
+        if (c->fast_kind == FK_CHEM)
+          MR_CUDA_TRY(c, launch_chem_chain(ccfg, a, *c->chemP, st));
+        else
+          MR_CUDA_TRY(c, launch_chain(cfg, a, c->chem, c->fastA, st));
         c->launches++;
         ycur[r] = c->y_work;
       }
-      on_work = true;
     }
     if (c0->profile) cudaEventRecord(pool_event(c0, timed.back().second + 1), st);
   }
-  (void)on_work;
 
   // combine failure keys (min over slabs / ranks)
   unsigned long long key = MR_NO_FAIL;
   if (n == 1 && c0->nranks > 1) {
-    MR_NCCL_TRY(c0, ncclAllReduce(c0->d_fail, c0->d_fail, 1, ncclUint64, ncclMin, c0->comm, st));
+    MR_NCCL_TRY(c0, AllReduce(c0->d_fail, c0->d_fail, 1, ncclUint64, ncclMin, c0->comm, st));
   }
   for (int r = 0; r < n; ++r) {
     MR_CUDA_TRY(cs[r], cudaMemcpyAsync(cs[r]->h_fail, cs[r]->d_fail, sizeof(unsigned long long),
@@ -839,13 +845,14 @@ void mr_ctx_destroy(mr_ctx* c)
   cudaStreamSynchronize(c->stream);
   free_state(c);
   for (void*& p : c->chem_bufs) free_dev(p);
+  delete c->chemP;
   free_dev_t(c->d_prof);
   free_dev_t(c->d_fail);
   free_dev_t(c->d_red);
   if (c->h_fail) cudaFreeHost(c->h_fail);
   if (c->h_red) cudaFreeHost(c->h_red);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
-  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm && nccl_api().ok) nccl_api().CommDestroy(c->comm);
   cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1003,6 +1010,100 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
   ch.RuP = kRu / kPatm;
   if (!ch.sp || !ch.rxn || !ch.rsp || !ch.csr_off || !ch.csr_ent)
     return set_err(c, MR_CUDA, "mr_fast_chemistry: device allocation failed");
+  // chemistry kernel parameters: per-species data in the constant bank,
+  // reaction records + production lists in a blob staged into shared memory
+  if (S + 1 > MR_CHEM_MAXS || R > MR_CHEM_MAXR)
+    return set_err(c, MR_CONTRACT, "mechanism too large for the chemistry kernel (S<=63)");
+  if (!c->chemP) c->chemP = new ChemParams();
+  ChemParams& P = *c->chemP;
+  std::memset(&P, 0, sizeof(P));
+  P.S = S;
+  P.R = R;
+  P.RuP = kRu / kPatm;
+  for (int k = 0; k < S; ++k) {
+    P.h0[k] = sp[0 * Sp + k]; P.a[k] = sp[1 * Sp + k]; P.hb[k] = sp[2 * Sp + k];
+    P.s0[k] = sp[3 * Sp + k]; P.rhoW[k] = sp[4 * Sp + k]; P.Wrho[k] = sp[5 * Sp + k];
+    P.c0[k] = sp[6 * Sp + k]; P.c1[k] = sp[7 * Sp + k]; P.c2[k] = sp[8 * Sp + k];
+  }
+  {
+    ChemCfg lay;
+    TableDev t4{};
+    t4.s = 4;
+    const int nnz = cnt[S];
+    // blob bound: records + entries + per-list padding (<= 3 per list)
+    const size_t blob_bound = (size_t)R * sizeof(ChemRec) +
+                              4 * ((size_t)nnz + 2 * 3 * (size_t)S * MR_CHEM_MAXCHUNK) + 16;
+    int rcz = 0, nch = 0;
+    if (chem_pick(&lay, S + 1, S, R, t4, 1) ||
+        chem_chunking(lay.NW, S, R, blob_bound, &rcz, &nch))
+      return set_err(c, MR_CONTRACT, "mechanism too large for the chemistry kernel's shared memory");
+    P.rc = rcz;
+    P.nchunk = nch;
+    {  // balanced component -> (warp, slot) assignment (LPT greedy, SPL slots per warp)
+      const int NW = lay.NW, SPL = lay.SPL;
+      std::vector<int> order(S + 1);
+      std::vector<double> cost(S + 1, 0.0);
+      for (int k = 0; k < S; ++k) cost[k] = 16.0 + (double)(cnt[k + 1] - cnt[k]);
+      for (int k = 0; k <= S; ++k) order[k] = k;
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cost[x] > cost[y]; });
+      std::vector<double> load(NW, 0.0);
+      std::vector<int> used(NW, 0);
+      for (int i = 0; i < MR_CHEM_MAXS; ++i) P.perm[i] = 255;
+      const bool identity = getenv("MR_CHEM_NOPERM") != nullptr;  // experiment hook
+      if (identity) {
+        for (int i = 0; i < NW * SPL && i <= S; ++i) P.perm[i] = (unsigned char)i;
+        order.clear();
+      }
+      for (int k : order) {
+        int best = -1;
+        for (int w2 = 0; w2 < NW; ++w2)
+          if (used[w2] < SPL && (best < 0 || load[w2] < load[best])) best = w2;
+        P.perm[best + NW * used[best]] = (unsigned char)k;
+        used[best]++;
+        load[best] += cost[k];
+      }
+    }
+    std::vector<ChemRec> recs(R);
+    for (int j = 0; j < R; ++j) {
+      ChemRec& r = recs[j];
+      std::memset(&r, 0, sizeof(r));
+      r.lnA = rx[j].x; r.beta = rx[j].y; r.EaR = rx[j].z;
+      r.r1o = (unsigned)rs[j].x * 512u; r.r2o = (unsigned)rs[j].y * 512u;
+      r.p1o = (unsigned)rs[j].z * 256u; r.p2o = (unsigned)rs[j].w * 256u;
+    }
+    const unsigned zero_off = (unsigned)rcz * 256u;  // all-zero row right after q
+    std::vector<unsigned> ents;
+    for (int k = 0; k < S; ++k)
+      for (int ch2 = 0; ch2 < nch; ++ch2) {
+        unsigned short st4[2], n4[2];
+        for (int sign = 0; sign < 2; ++sign) {  // 0: producing (+), 1: consuming (-)
+          while (ents.size() % 4) ents.push_back(zero_off);
+          st4[sign] = (unsigned short)(ents.size() / 4);
+          size_t n0 = ents.size();
+          for (int q2 = cnt[k]; q2 < cnt[k + 1]; ++q2) {
+            const int j = ent[q2] >> 1, prod = ent[q2] & 1;
+            if ((prod == 1) != (sign == 0)) continue;
+            if (j < ch2 * rcz || j >= (ch2 + 1) * rcz) continue;
+            ents.push_back((unsigned)(j - ch2 * rcz) * 256u);
+          }
+          while ((ents.size() - n0) % 4) ents.push_back(zero_off);
+          n4[sign] = (unsigned short)((ents.size() - n0) / 4);
+        }
+        P.lst[k][ch2] = make_ushort4(st4[0], n4[0], st4[1], n4[1]);
+      }
+    while (ents.size() % 4) ents.push_back(zero_off);
+    const size_t rec_bytes = (size_t)R * sizeof(ChemRec);
+    const size_t blob_bytes = rec_bytes + ents.size() * 4;
+    if (blob_bytes > blob_bound)
+      return set_err(c, MR_CONTRACT, "chemistry blob exceeds its shared-memory budget");
+    std::vector<unsigned char> blob(blob_bytes);
+    std::memcpy(blob.data(), recs.data(), rec_bytes);
+    std::memcpy(blob.data() + rec_bytes, ents.data(), ents.size() * 4);
+    P.blob = (const uint4*)up(blob.data(), blob_bytes);
+    if (!P.blob) return set_err(c, MR_CUDA, "mr_fast_chemistry: device allocation failed");
+    P.blob_words = (int)(blob_bytes / 16);
+    P.ent_base = (int)(rec_bytes / 16);
+  }
   c->chem = ch;
   c->S = S;
   c->R = R;
@@ -1205,13 +1306,23 @@ int mr_fast_rhs(mr_ctx* c, double t, const double* y, double* out)
   cudaSetDevice(c->device);
   int rc = ensure_scratch(c);
   if (rc) return rc;
-  ChainCfg cfg;
-  if (chain_pick(&cfg, c->fast_kind, c->ncomp, c->S, c->R, 4, 1))
-    return set_err(c, MR_CONTRACT, "unsupported component count");
   MR_CUDA_TRY(c, cudaMemcpyAsync(c->scr_in, y, c->dof * sizeof(double), cudaMemcpyHostToDevice,
                                  c->stream));
-  MR_CUDA_TRY(c, launch_fast_rhs(cfg, c->scr_in, c->scr_out, c->ncell, c->ncomp, c->chem,
-                                 c->fastA, c->stream));
+  if (c->fast_kind == FK_CHEM) {
+    ChemCfg ccfg;
+    TableDev t4{};
+    t4.s = 4;
+    if (chem_pick(&ccfg, c->ncomp, c->S, c->R, t4, 1))
+      return set_err(c, MR_CONTRACT, "unsupported mechanism size");
+    MR_CUDA_TRY(c, launch_chem_rhs(ccfg, c->scr_in, c->scr_out, c->ncell, c->ncomp, *c->chemP,
+                                   c->stream));
+  } else {
+    ChainCfg cfg;
+    if (chain_pick(&cfg, c->fast_kind, c->ncomp, c->S, c->R, 4, 1))
+      return set_err(c, MR_CONTRACT, "unsupported component count");
+    MR_CUDA_TRY(c, launch_fast_rhs(cfg, c->scr_in, c->scr_out, c->ncell, c->ncomp, c->chem,
+                                   c->fastA, c->stream));
+  }
   c->launches++;
   MR_CUDA_TRY(c, cudaMemcpyAsync(out, c->scr_out, c->dof * sizeof(double), cudaMemcpyDeviceToHost,
                                  c->stream));
@@ -1312,7 +1423,7 @@ int mr_nccl_unique_id(char* id128)
 {
   if (!id128) return MR_CONTRACT;
   ncclUniqueId id;
-  if (ncclGetUniqueId(&id) != ncclSuccess) return MR_CUDA;
+  if (!nccl_api().ok || nccl_api().GetUniqueId(&id) != ncclSuccess) return MR_CUDA;
   std::memcpy(id128, id.internal, NCCL_UNIQUE_ID_BYTES);
   return MR_OK;
 }
@@ -1328,7 +1439,7 @@ int mr_comm_init(mr_ctx* c, int nranks, int rank, const char* id128)
   }
   ncclUniqueId id;
   std::memcpy(id.internal, id128, NCCL_UNIQUE_ID_BYTES);
-  MR_NCCL_TRY(c, ncclCommInitRank(&c->comm, nranks, id, rank));
+  MR_NCCL_TRY(c, CommInitRank(&c->comm, nranks, id, rank));
   c->nranks = nranks;
   c->rank = rank;
   c->halo_elems = 0;  // reallocate halos with receive buffers
