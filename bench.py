@@ -316,7 +316,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--n", type=int, default=None, help="override grid size (debug)")
-    ap.add_argument("--sample-n", type=int, default=16, help="CPU baseline sub-grid size")
+    ap.add_argument("--sample-n", type=int, default=24, help="CPU baseline sub-grid size")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
