@@ -1,0 +1,114 @@
+// oracle/facade_test.cpp -- TEST INFRASTRUCTURE: compiles the C++ facade
+// (include/multirate_b200.hpp) against the reference's own headers and
+// sources and runs the same slow steps three ways:
+//   B: multirate::b200::mri_integrate   (device-resident product path)
+//   A: the reference's mri_integrate driving the GPU plugins through a
+//      reference PartitionedSystem ("Mode A", the drop-in callback route)
+//   C: the reference's mri_integrate with the CPU oracle physics
+// Built by `make -C oracle facade` into oracle/_ref/ (needs /root/reference).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+#include <string>
+
+#include "multirate/butcher.hpp"
+#include "multirate/mri.hpp"
+#include "multirate_b200.hpp"
+
+extern "C" {
+#include "mri_oracle.h"
+}
+
+using namespace multirate;
+
+namespace {
+double rel_err(const StateVector& a, const StateVector& b, int ncomp)
+{
+  const size_t nc = a.size() / ncomp;
+  double worst = 0.0;
+  for (int k = 0; k < ncomp; ++k) {
+    double d = 0.0, m = 0.0;
+    for (size_t i = 0; i < nc; ++i) {
+      d = std::max(d, std::fabs(a[k * nc + i] - b[k * nc + i]));
+      m = std::max(m, std::fabs(b[k * nc + i]));
+    }
+    worst = std::max(worst, m > 0 ? d / m : d);
+  }
+  return worst;
+}
+}  // namespace
+
+extern "C" int facade_selftest(int n, int S, int R, double rho, const double* species,
+                               const double* reactions, const int* rspecies, const double* y0in,
+                               const char* coupling, const char* table, int m, int order,
+                               double H, int steps, double* errs, uint64_t* counters, char* err,
+                               size_t errlen)
+{
+  try {
+    const int ncomp = S + 1;
+    const size_t dof = (size_t)n * n * n * ncomp;
+    StateVector y0(dof);
+    std::memcpy(y0.data(), y0in, dof * sizeof(double));
+    MriMethodConfig mc;
+    if (std::string(coupling).rfind("mri-coupling", 0) == 0) {
+      std::stringstream in{std::string(coupling)};
+      mc.coupling = import_coupling(in);
+    } else {
+      mc.coupling = register_coupling(coupling);
+    }
+    mc.fast_table = lookup_table(table);
+    mc.m = m;
+    const double u[3] = {1.0, 1.0, 1.0};
+
+    b200::Device dev(0);
+    dev.grid(n, n, n, ncomp);
+    dev.chemistry(S, R, rho, species, reactions, rspecies);
+    dev.stencil(order, 1e-3, u);
+
+    EvalCounters cB, cA, cC;
+    StateVector yB = b200::mri_integrate(dev, mc, 0.0, steps * H, H, y0, cB);
+    PartitionedSystem sysA = b200::partitioned_system(dev);
+    StateVector yA = mri_integrate(mc, sysA, ImplicitStageSolver{}, 0.0, steps * H, H, y0, cA);
+
+    orc_sys_cfg cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.n0 = cfg.n1 = cfg.n2 = n;
+    cfg.n0_global = n;
+    cfg.ncomp = ncomp;
+    cfg.length = 1.0;
+    cfg.fast_kind = ORC_FAST_CHEM;
+    cfg.slow_kind = ORC_SLOW_STENCIL;
+    cfg.S = S; cfg.R = R; cfg.rho = rho;
+    cfg.species = species; cfg.reactions = reactions; cfg.rspecies = rspecies;
+    cfg.order = order; cfg.diffusion = 1e-3; cfg.vel_kind = 0;
+    cfg.u_const[0] = cfg.u_const[1] = cfg.u_const[2] = 1.0;
+    cfg.threads = 1;
+    orc_sys* cs = orc_sys_create(&cfg);
+    PartitionedSystem sysC;
+    sysC.dimension = dof;
+    sysC.f_fast = [cs](double t, const StateVector& y) {
+      StateVector o(y.size());
+      orc_sys_fast_rhs(cs, t, y.data(), o.data());
+      return o;
+    };
+    sysC.f_explicit = [cs](double t, const StateVector& y) {
+      StateVector o(y.size());
+      orc_sys_slow_rhs(cs, t, y.data(), o.data());
+      return o;
+    };
+    StateVector yC = mri_integrate(mc, sysC, ImplicitStageSolver{}, 0.0, steps * H, H, y0, cC);
+    orc_sys_destroy(cs);
+
+    errs[0] = rel_err(yB, yC, ncomp);
+    errs[1] = rel_err(yA, yC, ncomp);
+    errs[2] = rel_err(yA, yB, ncomp);
+    b200::to_c(cB, counters);
+    b200::to_c(cA, counters + 8);
+    b200::to_c(cC, counters + 16);
+    return 0;
+  } catch (const std::exception& e) {
+    if (err && errlen) std::snprintf(err, errlen, "%s", e.what());
+    return 1;
+  }
+}

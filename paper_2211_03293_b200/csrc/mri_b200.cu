@@ -1109,17 +1109,16 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
   c->R = R;
   c->rho = rho;
   c->fast_kind = FK_CHEM;
-  // fp64 work per RHS evaluation: FMA = 2, +-*/ = 1,
-  // exp = log = 20 (DFMA-equivalents of the libdevice sequence, profiles/)
-  const double ce = 20.0;
+  // fp64 work per RHS evaluation + its RK4/forcing arithmetic (DESIGN.md
+  // "Roofline accounting"): FMA = 2, + - * / = 1, exp = 34 (the branch-free
+  // sequence of kernels_chem.cuh: 15 FMA + 1 add + 1 mul), log = 40.
+  const double ce = 34.0, cl = 40.0;
   double f = 0.0;
-  f += 6.0 * S + 2.0 + 1.0 + 1.0 + 1.0 + 2.0;  // e(T) sums, closed-form root
-  f += ce + 1.0;                               // log T, 1/T
-  f += S * (6.0 + ce + 1.0 + 1.0 + 1.0);       // g, exp, 1/E, C, W/rho
-  f += 2.0;                                    // RT/P and its inverse
-  int nnz = cnt[S];
-  for (int j = 0; j < R; ++j) f += 4.0 + ce + 5.0 + 5.0;  // kf, kr, q
-  f += nnz;                                               // production sums
+  f += 8.0 + cl + 3.0;                      // T(e) root, log T, 1/T, RT/P, P/RT
+  f += S * (6.0 + 6.0 + ce + 5.0 + 1.0);    // e(T) sums, g, exp, C/E'/D', W/rho
+  f += R * (4.0 + ce + 6.0);                // kf exponent, exp, forward/reverse, q
+  f += cnt[S];                              // production sums
+  f += (S + 1) * 7.0;                       // forcing Horner + f + r, stage, out
   c->chem_flops = f;
   return MR_OK;
 }
