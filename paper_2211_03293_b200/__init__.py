@@ -28,7 +28,7 @@ from . import tables
 from .configs import CONFIGS
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmri_b200.so")
+LIB_PATH = os.environ.get("MR_LIB_PATH", os.path.join(HERE, "libmri_b200.so"))  # override: A/B experiments
 COUPLING_DIR = os.path.join(HERE, "data", "couplings")
 
 MR_OK, MR_CONTRACT, MR_INTEGRATION, MR_CUDA = 0, 1, 2, 3

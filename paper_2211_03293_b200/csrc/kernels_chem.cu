@@ -19,11 +19,12 @@ MR_DECL(4, 3)
 MR_DECL(8, 3)
 MR_DECL(8, 7)
 MR_DECL(16, 4)
+MR_DECL(32, 2)
 #undef MR_DECL
 }  // namespace mrchem
 
 // (NW warps = slots, SPL components per thread) layouts
-#define MR_CHEM_BLOCK_LAYOUTS(X) X(4, 3) X(8, 3) X(8, 7) X(16, 4)
+#define MR_CHEM_BLOCK_LAYOUTS(X) X(4, 3) X(8, 3) X(8, 7) X(16, 4) X(32, 2)
 
 int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int ndeg)
 {
@@ -37,7 +38,7 @@ int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int nd
   cfg->ndeg = ndeg;
   if (ncomp <= 12) { cfg->NW = 4; cfg->SPL = 3; }
   else if (ncomp <= 24) { cfg->NW = 8; cfg->SPL = 3; }
-  else if (ncomp <= 64) { cfg->NW = 16; cfg->SPL = 4; }
+  else if (ncomp <= 64) { cfg->NW = 32; cfg->SPL = 2; }
   else return 1;
   if (const char* env = getenv("MR_CHEM_BLOCK")) {  // experiment hook "NW,SPL"
     int nw = 0, spl = 0;
@@ -56,7 +57,7 @@ int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int nd
 // fit the 227 KB shared memory of an SM (one block for NW = 16)
 int chem_chunking(int NW, int S, int R, size_t blob_bytes, int* rc, int* nchunk)
 {
-  const size_t budget = (size_t)(NW <= 8 ? 113 : 227) * 1024;
+  const size_t budget = (size_t)(NW <= 8 ? 113 : 227) * 1024;  // 2 blocks/SM for NW <= 8
   const size_t fixed = mrchem::smem_bytes(NW, S + 1, 0, (int)((blob_bytes + 15) / 16));
   if (fixed >= budget) return 1;
   int cap = (int)((budget - fixed) / 256);
