@@ -62,6 +62,16 @@ def test_slow_rhs_matches_oracle(name):
     assert per_species_rel_err(got, ref, cfg["S"] + 1) <= RHS_TOL
 
 
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_slow_rhs_tiled_kernel_matches_oracle(name):
+    """n1 % 8 == 0 and n2 % 32 == 0 selects the 2.5D shared-memory stencil."""
+    n = 32
+    ctx, cfg, y0 = gpu_ctx(name, n)
+    ref = oracle_physics(cfg, n).slow_rhs(y0)
+    got = ctx.slow_rhs(y0)
+    assert per_species_rel_err(got, ref, cfg["S"] + 1) <= RHS_TOL
+
+
 def test_slow_rhs_properties():
     """test_models.cpp:126-232 ported to 3D: constant -> 0, per-species
     telescoping conservation, linearity."""
@@ -328,11 +338,11 @@ def test_reductions_match_reference_definitions():
 
 
 # ------------------------------------------------------------- slabs
-@pytest.mark.parametrize("P_", [2, 4])
-def test_virtual_rank_slabs_equal_single_gpu_bitwise(P_):
+@pytest.mark.parametrize("P_,n", [(2, 16), (4, 16), (4, 32), (3, 32)])
+def test_virtual_rank_slabs_equal_single_gpu_bitwise(P_, n):
     """Slab decomposition (8th-order halos of 4 planes) on in-process virtual
-    ranks reproduces the single-slab result bit-for-bit."""
-    n = 16
+    ranks reproduces the single-slab result bit-for-bit (n = 32 exercises the
+    2.5D stencil's halo planes)."""
     one, cfg, y0 = gpu_ctx("C3", n)
     H = cfg["H"]
     one.mri_step(0.0, H)
