@@ -16,6 +16,10 @@
  *                                       (partitioned_system.hpp:25-61); the RHS
  *                                       callbacks become device "plugins"
  *   mr_fast_rhs / mr_slow_rhs        <- one RhsFn call (partitioned_system.hpp:17)
+ *   mr_slow_implicit_diffusion       <- PartitionedSystem::f_implicit + the
+ *                                       ImplicitStageSolver of IMEX couplings
+ *                                       (partitioned_system.hpp:25-61,
+ *                                        mri.cpp:378-421, solvers.cpp:34-208)
  *   mr_wrms_norm ... mr_all_finite   <- state_vector.hpp:119-176
  *   status codes                     <- ContractError / IntegrationError
  *                                       (state_vector.hpp:22-36)
@@ -104,6 +108,20 @@ int mr_slow_stencil(mr_ctx* ctx, int order, double diffusion, const double* u,
                     const double* vel_prof, int nmax);
 int mr_slow_linear(mr_ctx* ctx, const double* A);
 int mr_slow_none(mr_ctx* ctx);
+/* IMEX split of the slow partition (call after mr_slow_stencil): adds
+ * f_implicit = d_impl * L7 y (7-point periodic Laplacian, every component) and
+ * solves the ImplicitSolve stages (I - gamma f_implicit) Y = known with
+ * cg_iters iterations of Jacobi-preconditioned CG started at Y = known.
+ * Required by couplings with ImplicitSolve stages or gamma terms; explicit
+ * couplings on a split system are a ContractError (mri.cpp:310-319). */
+int mr_slow_implicit_diffusion(mr_ctx* ctx, double d_impl, int cg_iters);
+/* ImplicitStageSolver (mri.hpp:84-95) of the ImplicitSolve stages: the
+ * NewtonConfig (solvers.hpp:19-23; defaults 1e-10, 0.1, 10) and the WRMS
+ * weights (local slab, dof doubles, host; NULL = unit weights, freed when the
+ * grid changes).  Newton runs as newton_solve (solvers.cpp:150-208) with the
+ * fixed-iteration PCG in place of GMRES. */
+int mr_newton_config(mr_ctx* ctx, double tolerance, double safety, int max_iters,
+                     const double* weights);
 
 /* ---------------- state ---------------- */
 int mr_state_upload(mr_ctx* ctx, const double* host);   /* local slab, species-major */
@@ -131,6 +149,7 @@ int mr_last_failure(const mr_ctx* ctx, int* mri_stage, int* substep, int* inner_
  * Host buffers, local slab; slow evaluation exchanges halos when sharded. */
 int mr_fast_rhs(mr_ctx* ctx, double t, const double* y, double* out);
 int mr_slow_rhs(mr_ctx* ctx, double t, const double* y, double* out);
+int mr_implicit_rhs(mr_ctx* ctx, double t, const double* y, double* out);
 
 /* ---------------- reductions (device pointers, this context's stream) ---------------- */
 int mr_wrms_norm(mr_ctx* ctx, const double* x, const double* w, size_t n, double* out);

@@ -55,6 +55,13 @@ class OrcSysCfg(C.Structure):
         ("u_const", C.c_double * 3),
         ("prof", _dp), ("prof_nmax", C.c_int),
         ("threads", C.c_int),
+        ("imex", C.c_int),
+        ("d_impl", C.c_double),
+        ("cg_iters", C.c_int),
+        ("newton_tol", C.c_double),
+        ("newton_safety", C.c_double),
+        ("newton_max_iters", C.c_int),
+        ("newton_w", _dp),
     ]
 
 
@@ -89,7 +96,7 @@ def lib():
         L.orc_sys_create.argtypes = [C.POINTER(OrcSysCfg)]
         L.orc_sys_destroy.argtypes = [C.c_void_p]
         L.orc_sys_set_threads.argtypes = [C.c_void_p, C.c_int]
-        for fn in ("orc_sys_fast_rhs", "orc_sys_slow_rhs"):
+        for fn in ("orc_sys_fast_rhs", "orc_sys_slow_rhs", "orc_sys_implicit_rhs"):
             getattr(L, fn).argtypes = [C.c_void_p, C.c_double, _dp, _dp]
         L.orc_sys_initial_condition.argtypes = [C.c_void_p, C.c_uint64, _dp]
         for fn in ("orc_sys_mri_step",):
@@ -159,10 +166,11 @@ def velocity_profiles(seed: int, n0: int, n1: int, n2: int, length: float = 1.0)
 
 
 class StepError(RuntimeError):
-    def __init__(self, code, stage, msg):
+    def __init__(self, code, stage, msg, counters=None):
         super().__init__(msg)
         self.code = code
         self.stage = stage
+        self.counters = counters  # partial counts up to the failure
 
 
 class System:
@@ -172,7 +180,8 @@ class System:
     def __init__(self, n0, n1, n2, ncomp, *, length=1.0, fast="none", slow="none",
                  mech=None, S=0, R=0, rho=1e-3, fast_A=None, slow_A=None, order=2,
                  diffusion=0.0, u=(1.0, 1.0, 1.0), prof=None, n0_global=None, i0_global=0,
-                 threads=1):
+                 threads=1, imex=False, d_impl=0.0, cg_iters=0, newton=(1e-10, 0.1, 10),
+                 newton_weights=None):
         self._keep = []
         cfg = OrcSysCfg()
         cfg.n0, cfg.n1, cfg.n2 = n0, n1, n2
@@ -209,6 +218,16 @@ class System:
             cfg.vel_kind = 0
             cfg.u_const[:] = list(u)
         cfg.threads = threads
+        cfg.imex = int(imex)
+        cfg.d_impl = d_impl
+        cfg.cg_iters = cg_iters
+        # NewtonConfig (solvers.hpp:19-23) as run_method builds it from the
+        # StudyConfig defaults (harness.cpp:333-339, harness.hpp:59-61)
+        cfg.newton_tol, cfg.newton_safety, cfg.newton_max_iters = newton
+        if newton_weights is not None:
+            nw = np.ascontiguousarray(newton_weights, dtype=np.float64)
+            self._keep.append(nw)
+            cfg.newton_w = _ptr(nw)
         self.cfg = cfg
         self.ncell = n0 * n1 * n2
         self.ncomp = ncomp
@@ -239,6 +258,13 @@ class System:
         lib().orc_sys_slow_rhs(self.h, t, _ptr(y), _ptr(out))
         return out
 
+    def implicit_rhs(self, y, t=0.0):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        out = np.empty_like(y)
+        if lib().orc_sys_implicit_rhs(self.h, t, _ptr(y), _ptr(out)):
+            raise ValueError("implicit_rhs needs an IMEX system")
+        return out
+
     def initial_condition(self, seed):
         y = np.empty(self.dof)
         if lib().orc_sys_initial_condition(self.h, seed, _ptr(y)):
@@ -258,7 +284,7 @@ class System:
         rc, y2, cnt, stage, err = self._call(fn, coupling.encode(), fast_table.encode(), m, t, H,
                                              y=y, counters=counters)
         if rc:
-            raise StepError(rc, stage, err)
+            raise StepError(rc, stage, err, cnt)
         return y2, cnt
 
     def mri_integrate(self, coupling, fast_table, m, t0, tf, H, y, counters=None,
@@ -267,7 +293,7 @@ class System:
         rc, y2, cnt, stage, err = self._call(fn, coupling.encode(), fast_table.encode(), m, t0, tf,
                                              H, y=y, counters=counters)
         if rc:
-            raise StepError(rc, stage, err)
+            raise StepError(rc, stage, err, cnt)
         return y2, cnt
 
 

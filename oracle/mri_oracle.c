@@ -816,6 +816,44 @@ void orc_slow_rhs(const orc_problem* p, double t, const double* y, double* out)
   else memset(out, 0, sizeof(double) * dof);
 }
 
+/* f_implicit of the IMEX split: d_impl * L7 y, L7 = 7-point Laplacian
+ * (periodic; per axis (y+ + y-) - 2y over dx^2, axes summed in order) */
+typedef struct { const orc_grid* g; const double* Y; double* out; double scale; } lap_job;
+static void lap_range(void* pj, size_t lo, size_t hi)
+{
+  lap_job* jb = (lap_job*)pj;
+  const orc_grid* g = jb->g;
+  const int n[3] = {g->n0, g->n1, g->n2};
+  const size_t ncell = (size_t)g->n0 * g->n1 * g->n2;
+  const size_t strides[3] = {(size_t)g->n1 * g->n2, (size_t)g->n2, 1};
+  double inv_dx2[3];
+  for (int d = 0; d < 3; ++d) {
+    const double dx = g->length / n[d];
+    inv_dx2[d] = 1.0 / (dx * dx);
+  }
+  for (size_t idx = lo; idx < hi; ++idx) {
+    const size_t comp = idx / ncell, cell = idx % ncell;
+    const int co[3] = {(int)(cell / strides[0]), (int)((cell / strides[1]) % g->n1),
+                       (int)(cell % g->n2)};
+    const double* y = jb->Y + comp * ncell;
+    double lap = 0.0;
+    for (int d = 0; d < 3; ++d) {
+      const size_t base = cell - (size_t)co[d] * strides[d];
+      const double yp = y[base + (size_t)((co[d] + 1) % n[d]) * strides[d]];
+      const double ym = y[base + (size_t)((co[d] - 1 + n[d]) % n[d]) * strides[d]];
+      lap += ((yp + ym) - 2.0 * y[cell]) * inv_dx2[d];
+    }
+    jb->out[comp * ncell + cell] = jb->scale * lap;
+  }
+}
+
+void orc_implicit_rhs(const orc_problem* p, double t, const double* y, double* out)
+{
+  (void)t;
+  lap_job j = {p->grid, y, out, p->grid->d_impl};
+  parallel_for(p->ncell * (size_t)p->ncomp, p->threads, lap_range, &j);
+}
+
 /* ------------------------------------------------------------------ */
 /* Stepper                                                           */
 /* ------------------------------------------------------------------ */
@@ -871,9 +909,78 @@ static int erk_step_ws(const orc_table* tb, const forced_rhs* fr, double t, doub
 
 static int uses_implicit(const orc_coupling* cp) { return any_nonzero(cp->gamma, cp->ndeg_gamma, cp->s); }
 
-/* mri_step, proj/src/mri.cpp:323-435 (explicit and explicit-update stages;
- * ImplicitSolve stages are reported as a contract error: the IMEX path is
- * SURVEY.md 8(f) "next"). y is overwritten on success, untouched on error. */
+static double dotv(const double* a, const double* b, size_t n)
+{
+  double s = 0.0;
+  for (size_t i = 0; i < n; ++i) s += a[i] * b[i];
+  return s;
+}
+
+/* ImplicitSolve of the IMEX split: newton_solve (proj/src/solvers.cpp:150-208)
+ * on G(Y) = Y - gamma f_I(Y) - known from Y = known (WRMS weights newton_w), the
+ * linear solve (I - gamma d_impl L7) dY = -G done by cg_iters iterations of
+ * Jacobi-preconditioned CG from dY = 0, accumulated straight into Y.  Replaces
+ * gmres_solve (solvers.cpp:34-117) for this linear SPD stage operator
+ * (SURVEY.md 8(f)); the device runs the identical iteration.  Counters follow
+ * newton_solve: one implicit eval per residual, one nonlinear iteration per
+ * update; CG adds cg_iters linear iterations and cg_iters + 1 Jacobi
+ * applications per update.  Returns 1 when converged. */
+static int newton_pcg_stage(const orc_problem* p, double gamma, const double* known, double* Y,
+                            double* r, double* z, double* q, double* pv, orc_counters* cnt)
+{
+  const orc_grid* g = p->grid;
+  const size_t dof = p->ncell * (size_t)p->ncomp;
+  const int n[3] = {g->n0, g->n1, g->n2};
+  double sdx = 0.0;
+  for (int d = 0; d < 3; ++d) {
+    const double dx = g->length / n[d];
+    sdx += 2.0 / (dx * dx);
+  }
+  const double dg = 1.0 + gamma * (g->d_impl * sdx);
+  const double target = g->newton_safety * g->newton_tol;
+  memcpy(Y, known, sizeof(double) * dof);
+  for (int iter = 0; iter <= g->newton_max_iters; ++iter) {
+    orc_implicit_rhs(p, 0.0, Y, q);              /* residual (solvers.cpp:168-177) */
+    ++cnt->n_implicit_evals;
+    double ss = 0.0;
+    for (size_t i = 0; i < dof; ++i) {
+      double G = Y[i] + (-gamma) * q[i];
+      G = G + (-1.0) * known[i];
+      r[i] = -G;
+      const double Gw = g->newton_w ? G * g->newton_w[i] : G; /* wrms_norm, state_vector.hpp:119-129 */
+      ss += Gw * Gw;
+    }
+    const double wrms = sqrt(ss / (double)dof);
+    if (!isfinite(wrms)) return 0;
+    if (wrms <= target) return 1;
+    if (iter == g->newton_max_iters) break;
+    for (size_t i = 0; i < dof; ++i) z[i] = r[i] / dg;
+    memcpy(pv, z, sizeof(double) * dof);
+    double rz = dotv(r, z, dof);
+    for (int it = 0; it < g->cg_iters; ++it) {
+      orc_implicit_rhs(p, 0.0, pv, q);           /* q = A p = p - gamma f_I(p) */
+      for (size_t i = 0; i < dof; ++i) q[i] = pv[i] - gamma * q[i];
+      const double pAp = dotv(pv, q, dof);
+      const double alpha = pAp != 0.0 ? rz / pAp : 0.0;
+      for (size_t i = 0; i < dof; ++i) {
+        Y[i] = Y[i] + alpha * pv[i];
+        r[i] = r[i] - alpha * q[i];
+        z[i] = r[i] / dg;
+      }
+      const double rz_new = dotv(r, z, dof);
+      const double beta = rz != 0.0 ? rz_new / rz : 0.0;
+      for (size_t i = 0; i < dof; ++i) pv[i] = z[i] + beta * pv[i];
+      rz = rz_new;
+    }
+    cnt->n_linear_iters += (uint64_t)g->cg_iters;
+    cnt->n_precond_solves += (uint64_t)g->cg_iters + 1;
+    ++cnt->n_nonlinear_iters;
+  }
+  return 0;
+}
+
+/* mri_step, proj/src/mri.cpp:323-435.  ImplicitSolve stages use
+ * newton_pcg_stage.  y is overwritten on success, untouched on error. */
 int orc_mri_step(const orc_coupling* cp, const orc_table* fast, int m, const orc_problem* p,
                  double t, double* y, double H, orc_counters* cnt, int* fail_stage, char* err,
                  size_t errlen)
@@ -882,8 +989,14 @@ int orc_mri_step(const orc_coupling* cp, const orc_table* fast, int m, const orc
   if (H <= 0.0) { if (err) snprintf(err, errlen, "mri_step: H must be positive"); return ORC_CONTRACT; }
   const int s = cp->s;
   const size_t dof = p->ncell * (size_t)p->ncomp;
-  if (uses_implicit(cp)) {
-    if (err) snprintf(err, errlen, "mri_step: implicit couplings are outside the oracle's explicit path");
+  const int needs_implicit = uses_implicit(cp);
+  const int has_imp = p->slow_kind == ORC_SLOW_STENCIL && p->grid && p->grid->imex;
+  if (needs_implicit && !has_imp) {
+    if (err) snprintf(err, errlen, "mri_step: coupling needs f_implicit");
+    return ORC_CONTRACT;
+  }
+  if (!needs_implicit && has_imp) {
+    if (err) snprintf(err, errlen, "mri_step: explicit coupling on a split slow partition");
     return ORC_CONTRACT;
   }
   const int has_slow = p->slow_kind != ORC_SLOW_NONE; /* resolve_slow_explicit, mri.cpp:310-319 */
@@ -891,9 +1004,11 @@ int orc_mri_step(const orc_coupling* cp, const orc_table* fast, int m, const orc
   const int ndeg = d > 1 ? d : 1;
 
   double* fE[ORC_MAX_STAGES] = {0};
+  double* fI[ORC_MAX_STAGES] = {0};
   double* Y = (double*)malloc(sizeof(double) * dof);
   double* coeffs = (double*)malloc(sizeof(double) * dof * (size_t)ndeg);
   double* tmp = (double*)malloc(sizeof(double) * dof);
+  double* cgw = needs_implicit ? (double*)malloc(sizeof(double) * dof * 5) : NULL;
   erk_ws ws;
   for (int i = 0; i < fast->s; ++i) ws.k[i] = (double*)malloc(sizeof(double) * dof);
   ws.stage = (double*)malloc(sizeof(double) * dof);
@@ -908,26 +1023,37 @@ int orc_mri_step(const orc_coupling* cp, const orc_table* fast, int m, const orc
       orc_slow_rhs(p, t + cp->c[(j)] * H, Y, fE[(j)]);                   \
       ++cnt->n_explicit_evals;                                           \
     }                                                                    \
+    if (needs_implicit && cp->fI_referenced[(j)] &&                     \
+        cp->kind[(j)] != ORC_IMPLICIT_SOLVE) {                           \
+      if (!fI[(j)]) fI[(j)] = (double*)malloc(sizeof(double) * dof);    \
+      orc_implicit_rhs(p, t + cp->c[(j)] * H, Y, fI[(j)]);               \
+      ++cnt->n_implicit_evals;                                           \
+    }                                                                    \
   } while (0)
 
   EVAL_SLOW_AT(0);
   for (int i = 1; i < s && rc == ORC_OK; ++i) {
     const double dc = cp->c[i] - cp->c[i - 1];
     if (cp->kind[i] == ORC_FAST_IVP) {
-      /* build_forcing, mri.cpp:266-303 */
+      /* build_forcing, mri.cpp:266-303: gamma over fI, then omega over fE */
       memset(coeffs, 0, sizeof(double) * dof * (size_t)ndeg);
-      for (int k = 0; k < cp->ndeg_omega && rc == ORC_OK; ++k)
-        for (int j = 0; j < i; ++j) {
-          const double coef = cp->omega[k][i][j];
-          if (coef == 0.0) continue;
-          if (!fE[j]) {
-            if (err) snprintf(err, errlen, "build_forcing: missing explicit value at stage %d", j);
-            *fail_stage = i;
-            rc = ORC_INTEGRATION;
-            break;
+      for (int pass = 0; pass < 2 && rc == ORC_OK; ++pass) {
+        const int nd = pass == 0 ? cp->ndeg_gamma : cp->ndeg_omega;
+        for (int k = 0; k < nd && rc == ORC_OK; ++k)
+          for (int j = 0; j < i; ++j) {
+            const double coef = pass == 0 ? cp->gamma[k][i][j] : cp->omega[k][i][j];
+            if (coef == 0.0) continue;
+            double* h = pass == 0 ? fI[j] : fE[j];
+            if (!h) {
+              if (err) snprintf(err, errlen, "build_forcing: missing %s value at stage %d",
+                                pass == 0 ? "implicit" : "explicit", j);
+              *fail_stage = i;
+              rc = ORC_INTEGRATION;
+              break;
+            }
+            axpy_into(coeffs + (size_t)k * dof, coef / dc, h, dof);
           }
-          axpy_into(coeffs + (size_t)k * dof, coef / dc, fE[j], dof);
-        }
+      }
       if (rc != ORC_OK) break;
       forced_rhs fr = {p, ndeg, coeffs, t + cp->c[i - 1] * H, dc * H, tmp};
       long ns = lround((double)m * dc);
@@ -943,22 +1069,47 @@ int orc_mri_step(const orc_coupling* cp, const orc_table* fast, int m, const orc
       }
       if (rc != ORC_OK) break;
       ++cnt->n_fast_ivps;
-    } else if (cp->kind[i] == ORC_EXPLICIT_UPDATE) {
-      /* mri.cpp:380-384, :422-424 (known = Y + sum_j H(gbar fI + wbar fE)) */
-      for (int j = 0; j < i; ++j) {
+    } else {
+      /* mri.cpp:380-384: known = Y + sum_j H (gbar_ij fI_j + wbar_ij fE_j) */
+      for (int j = 0; j < i && rc == ORC_OK; ++j) {
+        if (cp->gbar[i][j] != 0.0) {
+          if (!fI[j]) { rc = ORC_CONTRACT; break; }
+          axpy_into(Y, H * cp->gbar[i][j], fI[j], dof);
+        }
         if (cp->wbar[i][j] != 0.0) {
-          if (!fE[j]) {
-            if (err) snprintf(err, errlen, "axpy_into: length mismatch");
-            rc = ORC_CONTRACT;
-            break;
-          }
+          if (!fE[j]) { rc = ORC_CONTRACT; break; }
           axpy_into(Y, H * cp->wbar[i][j], fE[j], dof);
         }
       }
-      if (rc != ORC_OK) break;
-    } else {
-      rc = ORC_CONTRACT;
-      break;
+      if (rc != ORC_OK) {
+        if (err) snprintf(err, errlen, "axpy_into: length mismatch");
+        break;
+      }
+      if (cp->kind[i] == ORC_IMPLICIT_SOLVE) {
+        if (!orc_all_finite(Y, dof)) { /* mri.cpp:386-390 */
+          if (err) snprintf(err, errlen, "mri_step: non-finite stage data at stage %d", i);
+          *fail_stage = i;
+          rc = ORC_INTEGRATION;
+          break;
+        }
+        const double gamma = H * cp->gbar[i][i];
+        double* known = cgw;
+        memcpy(known, Y, sizeof(double) * dof);
+        const int ok = newton_pcg_stage(p, gamma, known, Y, cgw + dof, cgw + 2 * dof,
+                                        cgw + 3 * dof, cgw + 4 * dof, cnt);
+        ++cnt->n_implicit_solves;
+        if (!ok) { /* mri.cpp:404-410 */
+          if (err) snprintf(err, errlen, "mri_step: nonlinear solve failed at stage %d", i);
+          *fail_stage = i;
+          rc = ORC_INTEGRATION;
+          break;
+        }
+        /* mri.cpp:418-421: fI_i = (Y - known) / gamma */
+        if (!fI[i]) fI[i] = (double*)malloc(sizeof(double) * dof);
+        memcpy(fI[i], Y, sizeof(double) * dof);
+        axpy_into(fI[i], -1.0, known, dof);
+        for (size_t q = 0; q < dof; ++q) fI[i][q] /= gamma;
+      }
     }
     if (!orc_all_finite(Y, dof)) { /* mri.cpp:427-431 */
       if (err) snprintf(err, errlen, "mri_step: non-finite state at stage %d", i);
@@ -970,9 +1121,9 @@ int orc_mri_step(const orc_coupling* cp, const orc_table* fast, int m, const orc
   }
 #undef EVAL_SLOW_AT
   if (rc == ORC_OK) memcpy(y, Y, sizeof(double) * dof);
-  for (int i = 0; i < s; ++i) free(fE[i]);
+  for (int i = 0; i < s; ++i) { free(fE[i]); free(fI[i]); }
   for (int i = 0; i < fast->s; ++i) free(ws.k[i]);
-  free(ws.stage); free(ws.out); free(Y); free(coeffs); free(tmp);
+  free(ws.stage); free(ws.out); free(Y); free(coeffs); free(tmp); free(cgw);
   return rc;
 }
 
@@ -1029,6 +1180,13 @@ orc_sys* orc_sys_create(const orc_sys_cfg* cfg)
   s->grid.order = cfg->order;
   s->grid.diffusion = cfg->diffusion;
   s->grid.vel_kind = cfg->vel_kind;
+  s->grid.imex = cfg->imex;
+  s->grid.d_impl = cfg->d_impl;
+  s->grid.cg_iters = cfg->cg_iters;
+  s->grid.newton_tol = cfg->newton_tol;
+  s->grid.newton_safety = cfg->newton_safety;
+  s->grid.newton_max_iters = cfg->newton_max_iters;
+  s->grid.newton_w = cfg->newton_w;
   for (int d = 0; d < 3; ++d) s->grid.u_const[d] = cfg->u_const[d];
   if (cfg->vel_kind == 1)
     for (int d = 0; d < 3; ++d)
@@ -1064,6 +1222,13 @@ int orc_sys_fast_rhs(orc_sys* s, double t, const double* y, double* out)
 int orc_sys_slow_rhs(orc_sys* s, double t, const double* y, double* out)
 {
   orc_slow_rhs(&s->prob, t, y, out);
+  return ORC_OK;
+}
+
+int orc_sys_implicit_rhs(orc_sys* s, double t, const double* y, double* out)
+{
+  if (!s->cfg.imex) return ORC_CONTRACT;
+  orc_implicit_rhs(&s->prob, t, y, out);
   return ORC_OK;
 }
 

@@ -119,6 +119,17 @@ typedef struct {
   /* vel_kind 1: u_d(cell) = P[d][0][coord of axis a0(d)] + P[d][1][coord of axis a1(d)],
    * a0 < a1 the two axes != d; profile arrays of length n_axis */
   const double* prof[3][2];
+  /* IMEX split (config C5): f_explicit = advection only (diffusion above must be
+   * 0), f_implicit = d_impl * L7 (7-point Laplacian); ImplicitSolve stages
+   * run newton_solve's iteration (solvers.cpp:150-208, unit weights) with
+   * cg_iters iterations of Jacobi-preconditioned CG as the linear solver */
+  int imex;
+  double d_impl;
+  int cg_iters;
+  double newton_tol;     /* NewtonConfig (solvers.hpp:19-23) */
+  double newton_safety;
+  int newton_max_iters;
+  const double* newton_w; /* ImplicitStageSolver::weights (mri.hpp:84-95); NULL = unit */
 } orc_grid;
 
 void orc_stencil_rhs(const orc_grid* g, const double* Y, double* out);
@@ -155,6 +166,7 @@ typedef struct {
 } orc_problem;
 
 void orc_fast_rhs(const orc_problem* p, double t, const double* y, double* out);
+void orc_implicit_rhs(const orc_problem* p, double t, const double* y, double* out);
 void orc_slow_rhs(const orc_problem* p, double t, const double* y, double* out);
 
 int orc_mri_step(const orc_coupling* cp, const orc_table* fast, int m,
@@ -186,6 +198,13 @@ typedef struct {
   const double* prof;    /* [3][2][prof_nmax] */
   int prof_nmax;
   int threads;
+  int imex;              /* 1: f_implicit = d_impl * L7, f_explicit = advection */
+  double d_impl;
+  int cg_iters;
+  double newton_tol;
+  double newton_safety;
+  int newton_max_iters;
+  const double* newton_w;
 } orc_sys_cfg;
 
 typedef struct orc_sys orc_sys;
@@ -195,6 +214,7 @@ const orc_problem* orc_sys_problem(const orc_sys* s);
 void orc_sys_set_threads(orc_sys* s, int threads);
 int orc_sys_fast_rhs(orc_sys* s, double t, const double* y, double* out);
 int orc_sys_slow_rhs(orc_sys* s, double t, const double* y, double* out);
+int orc_sys_implicit_rhs(orc_sys* s, double t, const double* y, double* out);
 int orc_sys_initial_condition(orc_sys* s, uint64_t seed, double* Y);
 /* coupling: registered name ("mis-kw3") or v1 audit text; fast table by name */
 int orc_sys_mri_step(orc_sys* s, const char* coupling, const char* fast_table, int m,

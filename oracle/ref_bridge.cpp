@@ -8,6 +8,8 @@
 // Used to (a) pin the C restatement in mri_oracle.c bit-for-bit, (b) export
 // the reference's coupling tables as v1 audit text (tests/golden/couplings),
 // and (c) time the reference CPU path in bench.py --impl reference.
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <sstream>
@@ -77,7 +79,45 @@ PartitionedSystem make_system(orc_sys* sys)
       return out;
     };
   }
+  if (p->grid && p->grid->imex) {  // f_implicit = d_impl L7, linear: J v = f_I(v)
+    ps.f_implicit = [sys](double t, const StateVector& y) {
+      StateVector out(y.size());
+      orc_sys_implicit_rhs(sys, t, y.data(), out.data());
+      return out;
+    };
+    ps.jv_implicit = [sys](double t, const StateVector&, const StateVector& v) {
+      StateVector out(v.size());
+      orc_sys_implicit_rhs(sys, t, v.data(), out.data());
+      return out;
+    };
+  }
   return ps;
+}
+
+// ImplicitStageSolver (mri.hpp:84-95) from the system's Newton settings --
+// the same NewtonConfig and WRMS weights the oracle and the device use.  The
+// GMRES settings only have to converge (the replacement linear solver is the
+// fixed-iteration PCG): tolerance relative to max|y| since the reacting-flow
+// state carries an energy component ~1e10.
+ImplicitStageSolver stage_solver(orc_sys* sys, const StateVector& y)
+{
+  const orc_grid* g = orc_sys_problem(sys)->grid;
+  ImplicitStageSolver s;
+  double ymax = 0.0;
+  for (double v : y) ymax = std::max(ymax, std::fabs(v));
+  if (g) {
+    s.newton.tolerance = g->newton_tol;
+    s.newton.safety = g->newton_safety;
+    s.newton.max_iters = g->newton_max_iters;
+    if (g->newton_w) {
+      s.weights = StateVector(y.size());
+      for (std::size_t i = 0; i < y.size(); ++i) s.weights[i] = g->newton_w[i];
+    }
+  }
+  s.gmres.tolerance = 1e-15 * (1.0 + ymax);
+  s.gmres.safety = 1.0;
+  s.gmres.max_iters = 200;
+  return s;
 }
 
 template <class Fn>
@@ -165,20 +205,21 @@ int ref_sys_mri_step(orc_sys* sys, const char* coupling, const char* fast_table,
                      double t, double H, double* y, uint64_t* counters, int* fail_stage,
                      char* err, size_t errlen)
 {
-  return guarded(err, errlen, fail_stage, [&] {
+  EvalCounters c = counters_from(counters);
+  const int rc = guarded(err, errlen, fail_stage, [&] {
     MriMethodConfig mc;
     mc.coupling = load_coupling(coupling);
     mc.fast_table = lookup_table(fast_table);
     mc.m = m;
     PartitionedSystem ps = make_system(sys);
-    EvalCounters c = counters_from(counters);
     StateVector yv(ps.dimension);
     std::memcpy(yv.data(), y, sizeof(double) * ps.dimension);
-    ImplicitStageSolver solver;
+    ImplicitStageSolver solver = stage_solver(sys, yv);
     StateVector out = mri_step(mc, ps, solver, t, yv, H, c);
     std::memcpy(y, out.data(), sizeof(double) * ps.dimension);
-    counters_to(c, counters);
-  }) ;
+  });
+  counters_to(c, counters);  // partial counts survive an exception, as in the reference
+  return rc;
 }
 
 int ref_sys_mri_integrate(orc_sys* sys, const char* coupling, const char* fast_table, int m,
@@ -194,7 +235,7 @@ int ref_sys_mri_integrate(orc_sys* sys, const char* coupling, const char* fast_t
     PartitionedSystem ps = make_system(sys);
     StateVector yv(ps.dimension);
     std::memcpy(yv.data(), y, sizeof(double) * ps.dimension);
-    ImplicitStageSolver solver;
+    ImplicitStageSolver solver = stage_solver(sys, yv);
     StateVector out = mri_integrate(mc, ps, solver, t0, tf, H, yv, c);
     std::memcpy(y, out.data(), sizeof(double) * ps.dimension);
   });

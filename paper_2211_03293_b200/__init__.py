@@ -25,7 +25,7 @@ import os
 import numpy as np
 
 from . import tables
-from .configs import CONFIGS
+from .configs import CONFIGS, stage_solver
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MR_LIB_PATH", os.path.join(HERE, "libmri_b200.so"))  # override: A/B experiments
@@ -91,6 +91,9 @@ def lib():
         "mr_slow_stencil": (C.c_int, [vp, C.c_int, C.c_double, _dp, _dp, C.c_int]),
         "mr_slow_linear": (C.c_int, [vp, _dp]),
         "mr_slow_none": (C.c_int, [vp]),
+        "mr_slow_implicit_diffusion": (C.c_int, [vp, C.c_double, C.c_int]),
+        "mr_implicit_rhs": (C.c_int, [vp, C.c_double, _dp, _dp]),
+        "mr_newton_config": (C.c_int, [vp, C.c_double, C.c_double, C.c_int, _dp]),
         "mr_state_upload": (C.c_int, [vp, _dp]),
         "mr_state_download": (C.c_int, [vp, _dp]),
         "mr_state_device_ptr": (C.c_void_p, [vp]),
@@ -307,6 +310,20 @@ class Context:
             uu = np.ascontiguousarray(u, dtype=np.float64)
             self._check(self.L.mr_slow_stencil(self.h, order, diffusion, _p(uu), None, 0))
 
+    def slow_implicit_diffusion(self, d_impl, cg_iters):
+        """IMEX split (after slow_stencil): f_implicit = d_impl * L7 y, solved
+        by cg_iters Jacobi-PCG iterations at ImplicitSolve stages."""
+        self._check(self.L.mr_slow_implicit_diffusion(self.h, d_impl, int(cg_iters)))
+
+    def newton_config(self, tolerance=1e-10, safety=0.1, max_iters=10, weights=None):
+        """ImplicitStageSolver.newton + weights (mri.hpp:84-95)."""
+        if weights is None:
+            self._check(self.L.mr_newton_config(self.h, tolerance, safety, int(max_iters), None))
+        else:
+            w = np.ascontiguousarray(weights, dtype=np.float64)
+            assert w.size == self.dof
+            self._check(self.L.mr_newton_config(self.h, tolerance, safety, int(max_iters), _p(w)))
+
     def slow_linear(self, A):
         a = np.ascontiguousarray(A, dtype=np.float64).ravel()
         self._check(self.L.mr_slow_linear(self.h, _p(a)))
@@ -370,6 +387,12 @@ class Context:
         y = np.ascontiguousarray(y, dtype=np.float64)
         out = np.empty_like(y)
         self._check(self.L.mr_slow_rhs(self.h, t, _p(y), _p(out)))
+        return out
+
+    def implicit_rhs(self, y, t=0.0):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        out = np.empty_like(y)
+        self._check(self.L.mr_implicit_rhs(self.h, t, _p(y), _p(out)))
         return out
 
     # ---- reductions over device pointers (state by default) ---------------
@@ -453,8 +476,8 @@ def slab_bounds(n0: int, nranks: int, rank: int):
 
 
 def setup_workload(ctx: Context, name: str, *, n=None, i0=0, n0_local=None, threads=0,
-                   make_state=True, config=None):
-    """Configure ctx for a BASELINE.json workload (C1-C4), optionally on a
+                   make_state=True, config=None, ymax=None):
+    """Configure ctx for a BASELINE.json workload (C1-C5), optionally on a
     smaller grid n and a slab [i0, i0+n0_local); returns (cfg, y0)."""
     cfg = dict(CONFIGS[name] if config is None else config)
     if n is not None:
@@ -471,9 +494,14 @@ def setup_workload(ctx: Context, name: str, *, n=None, i0=0, n0_local=None, thre
     else:
         ctx.slow_stencil(cfg["order"], cfg["diffusion"],
                          prof=velocity_profiles(cfg["vel_seed"], N, N, N))
+    if cfg.get("d_impl") is not None:
+        ctx.slow_implicit_diffusion(cfg["d_impl"], cfg["cg_iters"])
     y0 = None
     if make_state:
         y0 = initial_condition(cfg["ic_seed"], S, cfg["rho"], sp, N, N, N, 1.0, i0, n0l, threads)
         ctx.upload(y0)
+        if cfg.get("d_impl") is not None:
+            tol, safety, mx, w = stage_solver(y0, ymax)
+            ctx.newton_config(tol, safety, mx, w)
     cfg["mech"] = (sp, rx, rs)
     return cfg, y0

@@ -11,9 +11,9 @@
 
 #define MR_MAXS 6      // inner ERK stages (butcher tables up to cash-karp5)
 #define MR_MAXDEG 2    // forcing-polynomial coefficients (gark4 uses 2)
-#define MR_MAXREF 8    // referenced slow-RHS stage values per MRI stage
+#define MR_MAXREF 12   // referenced slow-RHS stage values per MRI stage
 #define MR_MAXCHAIN 6  // cell-local MRI stages fused into one launch
-#define MR_MAXSLOT 16  // stored slow-RHS stage values
+#define MR_MAXSLOT 24 // stored slow-RHS stage values
 #define MR_MAXLIN 8    // components of the linear test plugins
 
 // Explicit Butcher table (butcher.hpp:16-27)
@@ -124,6 +124,14 @@ struct StencilArgs {
   int nmax;
 };
 
+// 7-point Laplacian of the IMEX implicit partition (f_I = D L7 y)
+struct LapArgs {
+  int n0l, n1, n2, ncomp, M;  // M = halo depth of the exchanged planes
+  double inv_dx2[3];
+  double D;
+  double gamma, dg;           // stage gamma and the Jacobi diagonal 1 + gamma D sum 2/dx^2
+};
+
 enum FastKind { FK_NONE = 0, FK_CHEM = 1, FK_LINEAR = 2 };
 enum SlowKind { SK_NONE = 0, SK_STENCIL = 1, SK_LINEAR = 2 };
 
@@ -175,5 +183,20 @@ enum RedKind { RED_WRMS = 0, RED_TWO = 1, RED_DOT = 2, RED_MAX = 3, RED_NONFINIT
 cudaError_t launch_reduce(int kind, const double* x, const double* w, size_t n, double* d_part,
                           int nblocks, double* d_out, cudaStream_t st);
 int reduce_blocks();
+
+int lap_blocks();
+cudaError_t launch_lap7(int mode, const LapArgs& a, const double* y, const double* lo,
+                        const double* hi, const double* known, const double* w, double* o1,
+                        double* o2, double* o3, double* part, double* part2, cudaStream_t st);
+cudaError_t launch_cg_update(size_t n, double dg, const double* sc, double* Y, double* r, double* z,
+                             const double* p, const double* q, double* part, cudaStream_t st);
+cudaError_t launch_cg_p(size_t n, const double* sc, double* p, const double* z, cudaStream_t st);
+cudaError_t launch_part_sum(const double* part, double* sc, int slot, cudaStream_t st);
+cudaError_t launch_scalar_combine(double* const* scs, int n, int slot, cudaStream_t st);
+cudaError_t launch_gathered_sum(const double* g, int n, double* sc, int slot, cudaStream_t st);
+cudaError_t launch_scalar_copy(double* sc, int dst, int src, cudaStream_t st);
+cudaError_t launch_recover_fi(size_t n, double gamma, const double* Y, const double* known,
+                              double* fI, int mri_stage, unsigned long long* fail,
+                              cudaStream_t st);
 
 cudaError_t launch_fp64_peak(double* sink, int blocks, int threads, int iters, cudaStream_t st);

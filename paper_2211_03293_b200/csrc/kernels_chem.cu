@@ -19,12 +19,13 @@ MR_DECL(4, 3)
 MR_DECL(8, 3)
 MR_DECL(8, 7)
 MR_DECL(16, 4)
+MR_DECL(24, 3)
 MR_DECL(32, 2)
 #undef MR_DECL
 }  // namespace mrchem
 
 // (NW warps = slots, SPL components per thread) layouts
-#define MR_CHEM_BLOCK_LAYOUTS(X) X(4, 3) X(8, 3) X(8, 7) X(16, 4) X(32, 2)
+#define MR_CHEM_BLOCK_LAYOUTS(X) X(4, 3) X(8, 3) X(8, 7) X(16, 4) X(24, 3) X(32, 2)
 
 int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int ndeg)
 {

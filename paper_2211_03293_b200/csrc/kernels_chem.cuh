@@ -36,6 +36,11 @@
 
 namespace mrchem {
 
+#ifndef MR_RX_UNROLL
+#define MR_RX_UNROLL 2
+#endif
+constexpr int kRxUnroll = MR_RX_UNROLL;  // reaction-loop unroll (ILP)
+
 #ifndef MR_CHEM_PERM
 #define MR_KK(slot) (slot)
 #else
@@ -203,7 +208,7 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
     //      q = kf (C_r1 C_r2 - (D'_p1 D'_p2)(E'_r1 E'_r2)), kf = exp(lnA + beta lnT - EaR/T)
     char* qw = m.q + lane8 + (unsigned)w * 256u;
     const char* rp = m.rec + (j0 + w) * (int)sizeof(ChemRec);
-#pragma unroll 2
+#pragma unroll kRxUnroll
     for (int j = j0 + w; j < j1; j += NW) {
       const double2 ab = *reinterpret_cast<const double2*>(rp);
       const uint4 er = *reinterpret_cast<const uint4*>(rp + 16);
@@ -256,7 +261,7 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
 }
 
 template <int NW, int SPL, bool SUBDIAG, int MAXS, int NDEG>
-__global__ void __launch_bounds__(NW * 32, (NW <= 8 ? 2 : 1))
+__global__ void __launch_bounds__(NW * 32, (NW <= 8 ? 2 : 1))  // NW*32 threads: 1024 -> 64 regs
     chem_chain_kernel(const __grid_constant__ ChainArgs a, const __grid_constant__ ChemParams P)
 {
   extern __shared__ __align__(16) double smem_raw[];

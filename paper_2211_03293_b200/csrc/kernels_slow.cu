@@ -441,3 +441,257 @@ cudaError_t launch_fp64_peak(double* sink, int blocks, int threads, int iters, c
   fp64_peak_kernel<<<blocks, threads, 0, st>>>(sink, iters);
   return cudaGetLastError();
 }
+
+// ===========================================================================
+// IMEX slow-implicit partition (config C5): f_I = D L7 y and the fixed-
+// iteration Jacobi-preconditioned CG of the ImplicitSolve stages
+// (replaces newton_solve/gmres_solve, proj/src/solvers.cpp:34-208, for the
+// linear SPD stage operator I - gamma D L7; CPU form: oracle pcg_stage).
+// Dot products: per-block partials over a FIXED grid, combined in a fixed
+// order (and across slabs/ranks in rank order) -> bitwise reproducible.
+// ===========================================================================
+namespace {
+
+constexpr int kLapThreads = 256;
+constexpr int kLapBlocks = 592;
+
+__device__ __forceinline__ double lap7_at(const LapArgs& a, const double* __restrict__ y,
+                                          const double* lo, const double* hi, size_t comp,
+                                          size_t cell)
+{
+  const size_t plane = (size_t)a.n1 * a.n2;
+  const int i = (int)(cell / plane);
+  const size_t rem = cell - (size_t)i * plane;
+  const int j = (int)(rem / a.n2);
+  const int k = (int)(rem - (size_t)j * a.n2);
+  const size_t ncell = plane * a.n0l;
+  const double* yc = y + comp * ncell;
+  const double c0 = yc[cell];
+  // axis 0 through the halo planes (nearest: lo plane M-1, hi plane 0)
+  const double* lo_c = lo + comp * (size_t)a.M * plane;
+  const double* hi_c = hi + comp * (size_t)a.M * plane;
+  const double yp0 = i + 1 < a.n0l ? yc[cell + plane] : hi_c[rem];
+  const double ym0 = i > 0 ? yc[cell - plane] : lo_c[(size_t)(a.M - 1) * plane + rem];
+  const int jp = j + 1 < a.n1 ? j + 1 : 0, jm = j > 0 ? j - 1 : a.n1 - 1;
+  const int kp = k + 1 < a.n2 ? k + 1 : 0, km = k > 0 ? k - 1 : a.n2 - 1;
+  const size_t base = (size_t)i * plane;
+  const double yp1 = yc[base + (size_t)jp * a.n2 + k], ym1 = yc[base + (size_t)jm * a.n2 + k];
+  const double yp2 = yc[base + (size_t)j * a.n2 + kp], ym2 = yc[base + (size_t)j * a.n2 + km];
+  // same operation order as the oracle, no contraction
+  const double c2 = dmul(2.0, c0);
+  double lap = dmul(dadd(dadd(yp0, ym0), -c2), a.inv_dx2[0]);
+  lap = dadd(lap, dmul(dadd(dadd(yp1, ym1), -c2), a.inv_dx2[1]));
+  lap = dadd(lap, dmul(dadd(dadd(yp2, ym2), -c2), a.inv_dx2[2]));
+  return dmul(a.D, lap);
+}
+
+__device__ __forceinline__ void block_sum_store(double v, double* part)
+{
+  __shared__ double sh[kLapThreads];
+  __syncthreads();  // sh may still be read by a previous reduction
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = kLapThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+// MODE 0: o1 = D L7 y                                     (f_implicit evaluation)
+// MODE 1: Newton residual at Y = y (solvers.cpp:168-177):
+//         G = (Y - gamma D L7 Y) - known; r = -G; z = r/dg; p = z;
+//         partials sum (G w)^2 -> part, r.z -> part2
+// MODE 2: q = p - gamma D L7 p; partial p.q -> part        (CG matvec, y = p)
+template <int MODE>
+__global__ void __launch_bounds__(kLapThreads) lap7_kernel(const LapArgs a, const double* y,
+                                                           const double* lo, const double* hi,
+                                                           const double* known, const double* w,
+                                                           double* o1, double* o2, double* o3,
+                                                           double* part, double* part2)
+{
+  const size_t ncell = (size_t)a.n0l * a.n1 * a.n2;
+  const size_t n = ncell * a.ncomp;
+  double acc = 0.0, acc2 = 0.0;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t comp = idx / ncell, cell = idx - comp * ncell;
+    const double f = lap7_at(a, y, lo, hi, comp, cell);
+    if (MODE == 0) {
+      o1[idx] = f;
+    } else if (MODE == 1) {
+      double G = dadd(y[idx], dmul(-a.gamma, f));
+      G = dadd(G, dmul(-1.0, known[idx]));
+      const double r = -G;
+      const double z = r / a.dg;
+      o1[idx] = r;
+      o2[idx] = z;
+      o3[idx] = z;
+      const double Gw = w ? dmul(G, w[idx]) : G;
+      acc = dadd(acc, dmul(Gw, Gw));
+      acc2 = dadd(acc2, dmul(r, z));
+    } else {
+      const double pv = y[idx];
+      const double q = dadd(pv, -dmul(a.gamma, f));
+      o1[idx] = q;
+      acc = dadd(acc, dmul(pv, q));
+    }
+  }
+  if (MODE != 0) block_sum_store(acc, part);
+  if (MODE == 1) block_sum_store(acc2, part2);
+}
+
+// Y += alpha p; r -= alpha q; z = r/dg; partial r.z  (alpha = pAp != 0 ? rz/pAp : 0)
+__global__ void __launch_bounds__(kLapThreads) cg_update_kernel(size_t n, double dg,
+                                                                const double* sc, double* Y,
+                                                                double* r, double* z,
+                                                                const double* p, const double* q,
+                                                                double* part)
+{
+  const double rz = sc[0], pAp = sc[1];
+  const double alpha = pAp != 0.0 ? rz / pAp : 0.0;
+  double acc = 0.0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    Y[i] = dadd(Y[i], dmul(alpha, p[i]));
+    const double rr = dadd(r[i], -dmul(alpha, q[i]));
+    const double zz = rr / dg;
+    r[i] = rr;
+    z[i] = zz;
+    acc = dadd(acc, dmul(rr, zz));
+  }
+  block_sum_store(acc, part);
+}
+
+// p = z + beta p (beta = rz != 0 ? rz_new/rz : 0)
+__global__ void __launch_bounds__(kLapThreads) cg_p_kernel(size_t n, const double* sc, double* p,
+                                                           const double* z)
+{
+  const double rz = sc[0], rzn = sc[2];
+  const double beta = rz != 0.0 ? rzn / rz : 0.0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    p[i] = dadd(z[i], dmul(beta, p[i]));
+}
+
+// fixed-order sum of the block partials into sc[slot]
+__global__ void __launch_bounds__(1024) part_sum_kernel(const double* part, int np, double* sc,
+                                                        int slot)
+{
+  __shared__ double sh[1024];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sc[slot] = sh[0];
+}
+
+// global value = sum of the slabs' values in slab order, written to every slab
+struct ScalarSet {
+  int n;
+  double* sc[16];
+};
+__global__ void scalar_combine_kernel(const ScalarSet s, int slot)
+{
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double acc = 0.0;
+  for (int r = 0; r < s.n; ++r) acc += s.sc[r][slot];
+  for (int r = 0; r < s.n; ++r) s.sc[r][slot] = acc;
+}
+
+__global__ void gathered_sum_kernel(const double* g, int n, double* sc, int slot)
+{
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double acc = 0.0;
+  for (int r = 0; r < n; ++r) acc += g[r];
+  sc[slot] = acc;
+}
+
+__global__ void scalar_copy_kernel(double* sc, int dst, int src) { sc[dst] = sc[src]; }
+
+// fI_i = (Y - known) / gamma  (mri.cpp:418-421) + all_finite(Y) (mri.cpp:427-431)
+__global__ void __launch_bounds__(256) recover_fi_kernel(size_t n, double gamma, const double* Y,
+                                                         const double* known, double* fI,
+                                                         int mri_stage, unsigned long long* fail)
+{
+  bool bad = false;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const double y = Y[i];
+    fI[i] = dadd(y, -known[i]) / gamma;
+    bad |= !isfinite(y);
+  }
+  if (bad) atomicMin(fail, mr_fail_key(mri_stage, 0, 1));
+}
+
+}  // namespace
+
+int lap_blocks() { return kLapBlocks; }
+
+cudaError_t launch_lap7(int mode, const LapArgs& a, const double* y, const double* lo,
+                        const double* hi, const double* known, const double* w, double* o1,
+                        double* o2, double* o3, double* part, double* part2, cudaStream_t st)
+{
+  if (mode == 0)
+    lap7_kernel<0><<<kLapBlocks, kLapThreads, 0, st>>>(a, y, lo, hi, known, w, o1, o2, o3, part, part2);
+  else if (mode == 1)
+    lap7_kernel<1><<<kLapBlocks, kLapThreads, 0, st>>>(a, y, lo, hi, known, w, o1, o2, o3, part, part2);
+  else
+    lap7_kernel<2><<<kLapBlocks, kLapThreads, 0, st>>>(a, y, lo, hi, known, w, o1, o2, o3, part, part2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_update(size_t n, double dg, const double* sc, double* Y, double* r, double* z,
+                             const double* p, const double* q, double* part, cudaStream_t st)
+{
+  cg_update_kernel<<<kLapBlocks, kLapThreads, 0, st>>>(n, dg, sc, Y, r, z, p, q, part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_p(size_t n, const double* sc, double* p, const double* z, cudaStream_t st)
+{
+  cg_p_kernel<<<kLapBlocks, kLapThreads, 0, st>>>(n, sc, p, z);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_part_sum(const double* part, double* sc, int slot, cudaStream_t st)
+{
+  part_sum_kernel<<<1, 1024, 0, st>>>(part, kLapBlocks, sc, slot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scalar_combine(double* const* scs, int n, int slot, cudaStream_t st)
+{
+  ScalarSet s;
+  s.n = n;
+  for (int r = 0; r < n && r < 16; ++r) s.sc[r] = scs[r];
+  scalar_combine_kernel<<<1, 32, 0, st>>>(s, slot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gathered_sum(const double* g, int n, double* sc, int slot, cudaStream_t st)
+{
+  gathered_sum_kernel<<<1, 32, 0, st>>>(g, n, sc, slot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scalar_copy(double* sc, int dst, int src, cudaStream_t st)
+{
+  scalar_copy_kernel<<<1, 1, 0, st>>>(sc, dst, src);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_recover_fi(size_t n, double gamma, const double* Y, const double* known,
+                              double* fI, int mri_stage, unsigned long long* fail,
+                              cudaStream_t st)
+{
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks == 0) blocks = 1;
+  recover_fi_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, gamma, Y, known, fI, mri_stage, fail);
+  return cudaGetLastError();
+}

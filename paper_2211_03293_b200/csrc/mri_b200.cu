@@ -136,14 +136,15 @@ bool finalize(Coupling& cp, std::string& err)
 
 // ---------------------------------------------------------------------------
 struct Op {
-  enum Type { SLOW = 0, COUNT_SLOW = 1, CHAIN = 2, UPDATE = 3, MISSING = 4 } type;
+  enum Type { SLOW = 0, COUNT_SLOW = 1, CHAIN = 2, UPDATE = 3, MISSING = 4, IMPL = 5, SOLVE = 6 } type;
   int stage = 0;
   std::vector<int> stages;  // CHAIN
 };
 
 struct Plan {
   std::vector<Op> ops;
-  int slot_of[kMaxStages];
+  int slot_of[kMaxStages];   // fE_j
+  int islot_of[kMaxStages];  // fI_j (IMEX couplings)
   int nslots = 0;
 };
 
@@ -178,6 +179,21 @@ struct mr_ctx {
   int vel_kind = 0;
   double* d_prof = nullptr;
   int nmax = 0;
+  // IMEX implicit partition: f_I = d_impl L7, fixed-iteration PCG solves
+  bool imex = false;
+  double d_impl = 0.0;
+  int cg_iters = 0;
+  double *cg_known = nullptr, *cg_r = nullptr, *cg_z = nullptr, *cg_p = nullptr, *cg_q = nullptr;
+  double* cg_part = nullptr;    // block partials of a dot product
+  double* cg_part2 = nullptr;   // second set (the residual kernel reduces two sums)
+  double* cg_sc = nullptr;      // [0] rz, [1] pAp, [2] rz_new, [3] sum (G w)^2
+  double* cg_gather = nullptr;  // [nranks] for the cross-rank fixed-order sum
+  double* newton_w = nullptr;   // ImplicitStageSolver::weights (local slab); null = unit
+  double newton_tol = 1.0e-10;  // NewtonConfig defaults (solvers.hpp:19-23)
+  double newton_safety = 0.1;
+  int newton_max = 10;
+  int solve_evals[kMaxStages] = {};  // this step: residual evaluations per solve stage
+  int solve_nl[kMaxStages] = {};     // this step: Newton iterations per solve stage
   // buffers
   double* y_state = nullptr;
   double* y_work = nullptr;
@@ -251,8 +267,26 @@ void free_state(mr_ctx* c)
   free_dev_t(c->recv_hi);
   free_dev_t(c->scr_in);
   free_dev_t(c->scr_out);
+  free_dev_t(c->cg_known);
+  free_dev_t(c->cg_r);
+  free_dev_t(c->cg_z);
+  free_dev_t(c->cg_p);
+  free_dev_t(c->cg_q);
+  free_dev_t(c->newton_w);  // weights are per grid
   c->halo_elems = 0;
   c->state_valid = false;
+}
+
+int ensure_cg(mr_ctx* c)
+{
+  double** bufs[5] = {&c->cg_known, &c->cg_r, &c->cg_z, &c->cg_p, &c->cg_q};
+  for (double** b : bufs)
+    if (!*b) MR_CUDA_TRY(c, cudaMalloc(b, c->dof * sizeof(double)));
+  if (!c->cg_part) MR_CUDA_TRY(c, cudaMalloc(&c->cg_part, sizeof(double) * lap_blocks()));
+  if (!c->cg_part2) MR_CUDA_TRY(c, cudaMalloc(&c->cg_part2, sizeof(double) * lap_blocks()));
+  if (!c->cg_sc) MR_CUDA_TRY(c, cudaMalloc(&c->cg_sc, sizeof(double) * 8));
+  if (!c->cg_gather) MR_CUDA_TRY(c, cudaMalloc(&c->cg_gather, sizeof(double) * 64));
+  return MR_OK;
 }
 
 int ensure_state(mr_ctx* c)
@@ -306,10 +340,13 @@ int check_ready(mr_ctx* c)
     return set_err(c, MR_CONTRACT, "PartitionedSystem: fast/slow plugins not configured");
   if (c->fast_kind == FK_NONE && c->slow_kind == SK_NONE)
     return set_err(c, MR_CONTRACT, "PartitionedSystem: at least one partition required");
-  if (c->cp.implicit)
+  if (c->cp.implicit && !(c->slow_kind == SK_STENCIL && c->imex))
+    return set_err(c, MR_CONTRACT, "mri_step: coupling needs f_implicit");
+  if (!c->cp.implicit && c->imex)
     return set_err(c, MR_CONTRACT,
-                   "mri_step: coupling needs f_implicit (IMEX stages are not on the explicit "
-                   "device path yet)");
+                   "mri_step: explicit coupling on a split slow partition (f_I + f_E)");
+  if (c->imex && c->nranks > 16)
+    return set_err(c, MR_CONTRACT, "IMEX solves support at most 16 slabs per process group");
   if (c->fast_kind == FK_CHEM && c->ncomp != c->S + 1)
     return set_err(c, MR_CONTRACT, "chemistry plugin needs n_comp == S + 1");
   if ((c->fast_kind == FK_LINEAR && c->fastA.n != c->ncomp) ||
@@ -325,18 +362,34 @@ Plan build_plan(const mr_ctx* c)
   const Coupling& cp = c->cp;
   const int s = cp.s;
   Plan p;
-  for (int i = 0; i < kMaxStages; ++i) p.slot_of[i] = -1;
+  for (int i = 0; i < kMaxStages; ++i) p.slot_of[i] = p.islot_of[i] = -1;
   const bool slow = slow_present(c);
+  const bool imp = cp.implicit;  // check_ready guarantees the implicit plugin
   for (int j = 0; j < s; ++j)
     if (slow && cp.eval_at[j] && cp.fE_ref[j]) p.slot_of[j] = p.nslots++;
-  auto slow_op = [&](int j) {
-    if (!slow || !cp.eval_at[j]) return;
-    Op o;
-    o.type = p.slot_of[j] >= 0 ? Op::SLOW : Op::COUNT_SLOW;  // unreferenced: count only
-    o.stage = j;
-    p.ops.push_back(o);
+  for (int j = 0; j < s; ++j)
+    if (imp && cp.fI_ref[j]) p.islot_of[j] = p.nslots++;
+  // eval_slow_at (mri.cpp:339-349): f_E where scheduled, f_I where referenced
+  // (not at solve stages, whose f_I is recovered from the solve)
+  auto eval_ops = [&](int j) {
+    if (slow && cp.eval_at[j]) {
+      Op o;
+      o.type = p.slot_of[j] >= 0 ? Op::SLOW : Op::COUNT_SLOW;  // unreferenced: count only
+      o.stage = j;
+      p.ops.push_back(o);
+    }
+    if (imp && cp.fI_ref[j] && cp.kind[j] != MR_STAGE_IMPLICIT_SOLVE) {
+      Op o;
+      o.type = Op::IMPL;
+      o.stage = j;
+      p.ops.push_back(o);
+    }
   };
-  slow_op(0);
+  auto evals_at = [&](int j) {
+    return (slow && cp.eval_at[j]) ||
+           (imp && cp.fI_ref[j] && cp.kind[j] != MR_STAGE_IMPLICIT_SOLVE);
+  };
+  eval_ops(0);
   std::vector<int> run;
   auto flush = [&]() {
     if (run.empty()) return;
@@ -364,13 +417,15 @@ Plan build_plan(const mr_ctx* c)
     // fails inside build_forcing / axpy_into at that stage (mri.cpp:288-296)
     bool missing = false;
     for (int j = 0; j < i; ++j) {
-      bool refd = false;
+      bool refE = false, refI = false;
       if (cp.kind[i] == MR_STAGE_FAST_IVP) {
-        for (int k = 0; k < cp.ndeg_o; ++k) refd |= cp.W(k, i, j) != 0.0;
+        for (int k = 0; k < cp.ndeg_o; ++k) refE |= cp.W(k, i, j) != 0.0;
+        for (int k = 0; k < cp.ndeg_g; ++k) refI |= cp.G(k, i, j) != 0.0;
       } else {
-        refd = cp.wbar[i][j] != 0.0;
+        refE = cp.wbar[i][j] != 0.0;
+        refI = cp.gbar[i][j] != 0.0;
       }
-      if (refd && p.slot_of[j] < 0) missing = true;
+      if ((refE && p.slot_of[j] < 0) || (refI && p.islot_of[j] < 0)) missing = true;
     }
     if (missing) {
       flush();
@@ -380,10 +435,19 @@ Plan build_plan(const mr_ctx* c)
       p.ops.push_back(o);
       return p;
     }
-    run.push_back(i);
-    if ((slow && cp.eval_at[i]) || i == s - 1) {
+    if (cp.kind[i] == MR_STAGE_IMPLICIT_SOLVE) {
       flush();
-      slow_op(i);
+      Op o;
+      o.type = Op::SOLVE;
+      o.stage = i;
+      p.ops.push_back(o);
+      eval_ops(i);
+      continue;
+    }
+    run.push_back(i);
+    if (evals_at(i) || i == s - 1) {
+      flush();
+      eval_ops(i);
     }
   }
   return p;
@@ -422,22 +486,33 @@ void fill_chain_stage(const mr_ctx* c, int i, double t, double H, const Plan& p,
     st.t_start = sc.t_start;
     st.span = sc.span;
     st.h_sub = sc.h_sub;
-    for (int j = 0; j < i; ++j) {
-      bool refd = false;
-      for (int k = 0; k < cp.ndeg_o; ++k) refd |= cp.W(k, i, j) != 0.0;
-      if (!refd) continue;
-      const int r = st.nref++;
-      st.ref_slot[r] = p.slot_of[j];
-      for (int k = 0; k < MR_MAXDEG; ++k)
-        st.coef[k][r] = k < cp.ndeg_o ? cp.W(k, i, j) / sc.dc : 0.0;
+    // build_forcing order (mri.cpp:285-301): gamma over fI, then omega over fE
+    for (int pass = 0; pass < 2; ++pass) {
+      const int nd = pass == 0 ? cp.ndeg_g : cp.ndeg_o;
+      for (int j = 0; j < i; ++j) {
+        bool refd = false;
+        for (int k = 0; k < nd; ++k) refd |= (pass == 0 ? cp.G(k, i, j) : cp.W(k, i, j)) != 0.0;
+        if (!refd) continue;
+        const int r = st.nref++;
+        st.ref_slot[r] = pass == 0 ? p.islot_of[j] : p.slot_of[j];
+        for (int k = 0; k < MR_MAXDEG; ++k)
+          st.coef[k][r] = k < nd ? (pass == 0 ? cp.G(k, i, j) : cp.W(k, i, j)) / sc.dc : 0.0;
+      }
     }
   } else {
+    // known = Y + sum_j H (gbar_ij fI_j + wbar_ij fE_j), j ascending (mri.cpp:380-384)
     st.kind = 2;
     for (int j = 0; j < i; ++j) {
-      if (cp.wbar[i][j] == 0.0) continue;
-      const int r = st.nref++;
-      st.ref_slot[r] = p.slot_of[j];
-      st.coef[0][r] = H * cp.wbar[i][j];
+      if (cp.gbar[i][j] != 0.0) {
+        const int r = st.nref++;
+        st.ref_slot[r] = p.islot_of[j];
+        st.coef[0][r] = H * cp.gbar[i][j];
+      }
+      if (cp.wbar[i][j] != 0.0) {
+        const int r = st.nref++;
+        st.ref_slot[r] = p.slot_of[j];
+        st.coef[0][r] = H * cp.wbar[i][j];
+      }
     }
   }
 }
@@ -568,10 +643,25 @@ int eval_slow(mr_ctx** cs, int n, const double* const* ycur, double* const* outs
   return MR_OK;
 }
 
+void add_solve_counts(const mr_ctx* c, int stage, uint64_t* cnt)
+{
+  // newton_solve (solvers.cpp:150-208): one implicit eval per residual, one
+  // nonlinear iteration per update; each linear solve = cg_iters CG
+  // iterations (one matvec each) and cg_iters + 1 Jacobi applications
+  const uint64_t nl = (uint64_t)c->solve_nl[stage];
+  cnt[MR_CNT_IMPLICIT_EVALS] += (uint64_t)c->solve_evals[stage];
+  cnt[MR_CNT_NONLINEAR_ITERS] += nl;
+  cnt[MR_CNT_LINEAR_ITERS] += nl * (uint64_t)c->cg_iters;
+  cnt[MR_CNT_PRECOND_SOLVES] += nl * ((uint64_t)c->cg_iters + 1);
+  cnt[MR_CNT_IMPLICIT_SOLVES] += 1;
+}
+
 void add_counts_full(const mr_ctx* c, const Plan& p, double t, double H, uint64_t* cnt)
 {
   for (const Op& o : p.ops) {
     if (o.type == Op::SLOW || o.type == Op::COUNT_SLOW) cnt[MR_CNT_EXPLICIT_EVALS]++;
+    if (o.type == Op::IMPL) cnt[MR_CNT_IMPLICIT_EVALS]++;
+    if (o.type == Op::SOLVE) add_solve_counts(c, o.stage, cnt);
     if (o.type == Op::CHAIN)
       for (int i : o.stages)
         if (c->cp.kind[i] == MR_STAGE_FAST_IVP) {
@@ -583,13 +673,18 @@ void add_counts_full(const mr_ctx* c, const Plan& p, double t, double H, uint64_
 }
 
 // counts up to a failure at (stage, sub, inner) -- what the reference's
-// by-reference EvalCounters hold when mri_step throws
+// by-reference EvalCounters hold when mri_step throws.  For a solve stage,
+// inner 0 = non-finite stage data (before the solve), 1 = non-finite state
+// after it, 2 = Newton did not converge.
 void add_counts_partial(const mr_ctx* c, const Plan& p, double t, double H, int fs, int fsub,
                         int finner, uint64_t* cnt)
 {
   for (const Op& o : p.ops) {
     if ((o.type == Op::SLOW || o.type == Op::COUNT_SLOW) && o.stage < fs)
       cnt[MR_CNT_EXPLICIT_EVALS]++;
+    if (o.type == Op::IMPL && o.stage < fs) cnt[MR_CNT_IMPLICIT_EVALS]++;
+    if (o.type == Op::SOLVE && (o.stage < fs || (o.stage == fs && finner >= 1)))
+      add_solve_counts(c, o.stage, cnt);
     if (o.type == Op::CHAIN)
       for (int i : o.stages) {
         if (c->cp.kind[i] != MR_STAGE_FAST_IVP || i > fs) continue;
@@ -602,6 +697,166 @@ void add_counts_partial(const mr_ctx* c, const Plan& p, double t, double H, int 
         }
       }
   }
+}
+
+LapArgs lap_args(const mr_ctx* c, double gamma)
+{
+  LapArgs a{};
+  a.n0l = c->n0l;
+  a.n1 = c->n1;
+  a.n2 = c->n2;
+  a.ncomp = c->ncomp;
+  a.M = c->M;
+  const int ng[3] = {c->n0, c->n1, c->n2};
+  double sdx = 0.0;
+  for (int d = 0; d < 3; ++d) {
+    const double dx = c->length / ng[d];
+    a.inv_dx2[d] = 1.0 / (dx * dx);
+    sdx += 2.0 / (dx * dx);
+  }
+  a.D = c->d_impl;
+  a.gamma = gamma;
+  a.dg = 1.0 + gamma * (c->d_impl * sdx);
+  return a;
+}
+
+// f_I = d_impl L7 y of every context's current state into `outs`
+int eval_implicit(mr_ctx** cs, int n, const double* const* ycur, double* const* outs,
+                  cudaStream_t st)
+{
+  std::vector<const double*> lo(n), hi(n);
+  int rc = exchange_halos(cs, n, ycur, lo.data(), hi.data(), st);
+  if (rc) return rc;
+  for (int r = 0; r < n; ++r) {
+    MR_CUDA_TRY(cs[r], launch_lap7(0, lap_args(cs[r], 0.0), ycur[r], lo[r], hi[r], nullptr,
+                                   nullptr, outs[r], nullptr, nullptr, nullptr, nullptr, st));
+    cs[r]->launches++;
+  }
+  return MR_OK;
+}
+
+// global dot product: block partials -> per-slab value -> sum over slabs
+// (in-process, slab order) or ranks (NCCL all-gather, rank order)
+int dot_finalize(mr_ctx** cs, int n, int slot, cudaStream_t st, bool second = false)
+{
+  for (int r = 0; r < n; ++r) {
+    MR_CUDA_TRY(cs[r], launch_part_sum(second ? cs[r]->cg_part2 : cs[r]->cg_part, cs[r]->cg_sc,
+                                       slot, st));
+    cs[r]->launches++;
+  }
+  if (n > 1) {
+    std::vector<double*> scs(n);
+    for (int r = 0; r < n; ++r) scs[r] = cs[r]->cg_sc;
+    MR_CUDA_TRY(cs[0], launch_scalar_combine(scs.data(), n, slot, st));
+    cs[0]->launches++;
+  } else if (cs[0]->nranks > 1) {
+    mr_ctx* c = cs[0];
+    MR_NCCL_TRY(c, AllGather(c->cg_sc + slot, c->cg_gather, 1, ncclDouble, c->comm, st));
+    MR_CUDA_TRY(c, launch_gathered_sum(c->cg_gather, c->nranks, c->cg_sc, slot, st));
+    c->launches++;
+  }
+  return MR_OK;
+}
+
+// ImplicitSolve stage i (mri.cpp:378-421): known, then newton_solve
+// (solvers.cpp:150-208) from Y = known with the fixed-iteration PCG as the
+// linear solver (same iteration as oracle newton_pcg_stage), then
+// fI_i = (Y - known)/gamma.  The convergence test is a host decision on the
+// globally reduced WRMS (one 8-byte read per Newton iteration; every slab and
+// rank sees the same value).  *host_key is set when Newton fails.
+int solve_stage(mr_ctx** cs, int n, int i, double t, double H, const Plan& plan,
+                std::vector<const double*>& ycur, cudaStream_t st, unsigned long long* host_key)
+{
+  mr_ctx* c0 = cs[0];
+  const double gamma = H * c0->cp.gbar[i][i];
+  const double target = c0->newton_safety * c0->newton_tol;
+  const double nglob = (double)c0->n0 * c0->n1 * c0->n2 * c0->ncomp;
+  std::vector<const double*> lo(n), hi(n), src(n);
+  for (int r = 0; r < n; ++r) {
+    mr_ctx* c = cs[r];
+    int rc = ensure_cg(c);
+    if (rc) return rc;
+    ChainStageDev sd;
+    fill_chain_stage(c, i, t, H, plan, sd);
+    const double* f[MR_MAXREF];
+    for (int q = 0; q < sd.nref; ++q) f[q] = c->slots[sd.ref_slot[q]];
+    MR_CUDA_TRY(c, launch_update(ycur[r], c->cg_known, sd.nref, f, sd.coef[0], c->dof, i,
+                                 c->d_fail, st));
+    MR_CUDA_TRY(c, cudaMemcpyAsync(c->y_work, c->cg_known, c->dof * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, st));
+    c->launches++;
+    ycur[r] = c->y_work;
+    c->solve_evals[i] = 0;
+    c->solve_nl[i] = 0;
+  }
+  bool converged = false;
+  for (int iter = 0; iter <= c0->newton_max; ++iter) {
+    // residual G(Y) at Y = y_work; r = -G, z = r/dg, p = z
+    for (int r = 0; r < n; ++r) src[r] = cs[r]->y_work;
+    int rc = exchange_halos(cs, n, src.data(), lo.data(), hi.data(), st);
+    if (rc) return rc;
+    for (int r = 0; r < n; ++r) {
+      mr_ctx* c = cs[r];
+      MR_CUDA_TRY(c, launch_lap7(1, lap_args(c, gamma), c->y_work, lo[r], hi[r], c->cg_known,
+                                 c->newton_w, c->cg_r, c->cg_z, c->cg_p, c->cg_part, c->cg_part2,
+                                 st));
+      c->launches++;
+      c->solve_evals[i]++;
+    }
+    rc = dot_finalize(cs, n, 3, st);
+    if (rc) return rc;
+    MR_CUDA_TRY(c0, cudaMemcpyAsync(c0->h_red, c0->cg_sc + 3, sizeof(double),
+                                    cudaMemcpyDeviceToHost, st));
+    MR_CUDA_TRY(c0, cudaStreamSynchronize(st));
+    const double wrms = std::sqrt(c0->h_red[0] / nglob);
+    if (!std::isfinite(wrms)) break;
+    if (wrms <= target) {
+      converged = true;
+      break;
+    }
+    if (iter == c0->newton_max) break;
+    rc = dot_finalize(cs, n, 0, st, true);  // rz
+    if (rc) return rc;
+    for (int it = 0; it < c0->cg_iters; ++it) {
+      for (int r = 0; r < n; ++r) src[r] = cs[r]->cg_p;
+      rc = exchange_halos(cs, n, src.data(), lo.data(), hi.data(), st);
+      if (rc) return rc;
+      for (int r = 0; r < n; ++r) {
+        mr_ctx* c = cs[r];
+        MR_CUDA_TRY(c, launch_lap7(2, lap_args(c, gamma), c->cg_p, lo[r], hi[r], nullptr, nullptr,
+                                   c->cg_q, nullptr, nullptr, c->cg_part, nullptr, st));
+        c->launches++;
+      }
+      rc = dot_finalize(cs, n, 1, st);  // pAp
+      if (rc) return rc;
+      for (int r = 0; r < n; ++r) {
+        mr_ctx* c = cs[r];
+        MR_CUDA_TRY(c, launch_cg_update(c->dof, lap_args(c, gamma).dg, c->cg_sc, c->y_work,
+                                        c->cg_r, c->cg_z, c->cg_p, c->cg_q, c->cg_part, st));
+        c->launches++;
+      }
+      rc = dot_finalize(cs, n, 2, st);  // rz_new
+      if (rc) return rc;
+      for (int r = 0; r < n; ++r) {
+        mr_ctx* c = cs[r];
+        MR_CUDA_TRY(c, launch_cg_p(c->dof, c->cg_sc, c->cg_p, c->cg_z, st));
+        MR_CUDA_TRY(c, launch_scalar_copy(c->cg_sc, 0, 2, st));
+        c->launches += 2;
+      }
+    }
+    for (int r = 0; r < n; ++r) cs[r]->solve_nl[i]++;
+  }
+  if (!converged) {
+    *host_key = mr_fail_key(i, 0, 2);
+    return MR_OK;
+  }
+  for (int r = 0; r < n; ++r) {
+    mr_ctx* c = cs[r];
+    double* fI = plan.islot_of[i] >= 0 ? c->slots[plan.islot_of[i]] : c->cg_q;
+    MR_CUDA_TRY(c, launch_recover_fi(c->dof, gamma, c->y_work, c->cg_known, fI, i, c->d_fail, st));
+    c->launches++;
+  }
+  return MR_OK;
 }
 
 // One slow step over a domain of slab contexts sharing a device stream (n > 1)
@@ -618,6 +873,24 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
     if (rc) return rc;
   }
   const Plan plan = build_plan(c0);
+  if (plan.nslots > MR_MAXSLOT)
+    return set_err(c0, MR_CONTRACT, "coupling stores more slow stage values than the device plan holds");
+  for (int i = 1; i < c0->cp.s; ++i) {
+    int nref = 0;
+    const Coupling& cp = c0->cp;
+    for (int j = 0; j < i; ++j) {
+      bool g = false, w = false;
+      for (int k = 0; k < cp.ndeg_g; ++k) g |= cp.G(k, i, j) != 0.0;
+      for (int k = 0; k < cp.ndeg_o; ++k) w |= cp.W(k, i, j) != 0.0;
+      if (cp.kind[i] != MR_STAGE_FAST_IVP) {
+        g = cp.gbar[i][j] != 0.0;
+        w = cp.wbar[i][j] != 0.0;
+      }
+      nref += (int)g + (int)w;
+    }
+    if (nref > MR_MAXREF)
+      return set_err(c0, MR_CONTRACT, "coupling stage references more slow values than the device plan holds");
+  }
   for (int r = 0; r < n; ++r) {
     int rc = ensure_slots(cs[r], plan.nslots);
     if (rc) return rc;
@@ -640,6 +913,7 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
   size_t ev = 0;
   std::vector<std::pair<int, size_t>> timed;  // (class, event index)
   int missing_stage = -1;
+  unsigned long long host_key = MR_NO_FAIL;  // Newton failure (host decision)
 
   for (const Op& o : plan.ops) {
     if (o.type == Op::COUNT_SLOW) continue;
@@ -647,7 +921,7 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
       missing_stage = o.stage;
       break;
     }
-    const int cls = o.type == Op::CHAIN ? 0 : (o.type == Op::SLOW ? 1 : 2);
+    const int cls = o.type == Op::CHAIN ? 0 : (o.type == Op::SLOW || o.type == Op::IMPL || o.type == Op::SOLVE ? 1 : 2);
     if (c0->profile) {
       cudaEventRecord(pool_event(c0, ev), st);
       timed.push_back({cls, ev});
@@ -657,6 +931,17 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
       for (int r = 0; r < n; ++r) outs[r] = cs[r]->slots[plan.slot_of[o.stage]];
       int rc = eval_slow(cs, n, ycur.data(), outs.data(), st);
       if (rc) return rc;
+    } else if (o.type == Op::IMPL) {
+      for (int r = 0; r < n; ++r) outs[r] = cs[r]->slots[plan.islot_of[o.stage]];
+      int rc = eval_implicit(cs, n, ycur.data(), outs.data(), st);
+      if (rc) return rc;
+    } else if (o.type == Op::SOLVE) {
+      int rc = solve_stage(cs, n, o.stage, t, H, plan, ycur, st, &host_key);
+      if (rc) return rc;
+      if (host_key != MR_NO_FAIL) {
+        if (c0->profile) cudaEventRecord(pool_event(c0, timed.back().second + 1), st);
+        break;
+      }
     } else if (o.type == Op::UPDATE) {
       for (int r = 0; r < n; ++r) {
         mr_ctx* c = cs[r];
@@ -706,6 +991,7 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
   }
   MR_CUDA_TRY(c0, cudaStreamSynchronize(st));
   for (int r = 0; r < n; ++r) key = std::min(key, *cs[r]->h_fail);
+  key = std::min(key, host_key);
 
   if (c0->profile) {
     c0->prof_chem = c0->prof_slow = c0->prof_other = 0.0;
@@ -741,7 +1027,7 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
     const int finner = (int)(key & 0xFFull);
     uint64_t part[8] = {};
     const bool ivp = c0->cp.kind[fs] == MR_STAGE_FAST_IVP;
-    add_counts_partial(c0, plan, t, H, fs, ivp ? fsub : 0, ivp ? finner : 0, part);
+    add_counts_partial(c0, plan, t, H, fs, ivp ? fsub : 0, finner, part);
     if (counters)
       for (int q = 0; q < 8; ++q) counters[q] += part[q];
     for (int r = 0; r < n; ++r) {
@@ -754,6 +1040,12 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
       return set_err(c0, MR_INTEGRATION,
                      finner == c0->tab.s ? "erk_step: non-finite result"
                                          : "erk_step: non-finite stage value");
+    if (c0->cp.kind[fs] == MR_STAGE_IMPLICIT_SOLVE && finner == 0)
+      return set_err(c0, MR_INTEGRATION,
+                     "mri_step: non-finite stage data at stage " + std::to_string(fs));
+    if (c0->cp.kind[fs] == MR_STAGE_IMPLICIT_SOLVE && finner == 2)
+      return set_err(c0, MR_INTEGRATION,
+                     "mri_step: nonlinear solve failed at stage " + std::to_string(fs));
     return set_err(c0, MR_INTEGRATION, "mri_step: non-finite state at stage " + std::to_string(fs));
   }
   if (counters) add_counts_full(c0, plan, t, H, counters);
@@ -849,6 +1141,10 @@ void mr_ctx_destroy(mr_ctx* c)
   free_dev_t(c->d_prof);
   free_dev_t(c->d_fail);
   free_dev_t(c->d_red);
+  free_dev_t(c->cg_part);
+  free_dev_t(c->cg_part2);
+  free_dev_t(c->cg_sc);
+  free_dev_t(c->cg_gather);
   if (c->h_fail) cudaFreeHost(c->h_fail);
   if (c->h_red) cudaFreeHost(c->h_red);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -1163,6 +1459,7 @@ int mr_slow_stencil(mr_ctx* c, int order, double diffusion, const double* u, con
     c->vel_kind = 0;
   }
   c->slow_kind = SK_STENCIL;
+  c->imex = false;  // mr_slow_implicit_diffusion adds the implicit partition
   c->halo_elems = 0;
   free_dev_t(c->send_lo);
   free_dev_t(c->send_hi);
@@ -1171,10 +1468,62 @@ int mr_slow_stencil(mr_ctx* c, int order, double diffusion, const double* u, con
   return MR_OK;
 }
 
+static int ensure_scratch(mr_ctx* c);
+
+int mr_slow_implicit_diffusion(mr_ctx* c, double d_impl, int cg_iters)
+{
+  if (!c || c->slow_kind != SK_STENCIL || !(d_impl >= 0.0) || cg_iters < 0)
+    return set_err(c, MR_CONTRACT,
+                   "mr_slow_implicit_diffusion: needs the stencil plugin, d_impl >= 0, cg_iters >= 0");
+  c->imex = true;
+  c->d_impl = d_impl;
+  c->cg_iters = cg_iters;
+  return MR_OK;
+}
+
+int mr_newton_config(mr_ctx* c, double tolerance, double safety, int max_iters,
+                     const double* weights)
+{
+  if (!c || !(tolerance > 0.0) || !(safety > 0.0) || safety > 1.0 || max_iters < 0)
+    return set_err(c, MR_CONTRACT, "newton_solve: bad NewtonConfig");
+  if (weights && !c->has_grid) return set_err(c, MR_CONTRACT, "grid not set (mr_grid_set)");
+  cudaSetDevice(c->device);
+  c->newton_tol = tolerance;
+  c->newton_safety = safety;
+  c->newton_max = max_iters;
+  free_dev_t(c->newton_w);
+  if (weights) {
+    MR_CUDA_TRY(c, cudaMalloc(&c->newton_w, c->dof * sizeof(double)));
+    MR_CUDA_TRY(c, cudaMemcpy(c->newton_w, weights, c->dof * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  return MR_OK;
+}
+
+int mr_implicit_rhs(mr_ctx* c, double t, const double* y, double* out)
+{
+  (void)t;
+  if (!c || !y || !out) return MR_CONTRACT;
+  if (!c->imex) return set_err(c, MR_CONTRACT, "mr_implicit_rhs: no implicit partition configured");
+  cudaSetDevice(c->device);
+  int rc = ensure_scratch(c);
+  if (rc) return rc;
+  MR_CUDA_TRY(c, cudaMemcpyAsync(c->scr_in, y, c->dof * sizeof(double), cudaMemcpyHostToDevice,
+                                 c->stream));
+  const double* ycur = c->scr_in;
+  double* o = c->scr_out;
+  rc = eval_implicit(&c, 1, &ycur, &o, c->stream);
+  if (rc) return rc;
+  MR_CUDA_TRY(c, cudaMemcpyAsync(out, c->scr_out, c->dof * sizeof(double), cudaMemcpyDeviceToHost,
+                                 c->stream));
+  MR_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MR_OK;
+}
+
 int mr_slow_linear(mr_ctx* c, const double* A)
 {
   if (!c || !A || !c->has_grid || c->ncomp > MR_MAXLIN)
     return set_err(c, MR_CONTRACT, "mr_slow_linear: needs grid with n_comp <= 8");
+  c->imex = false;
   c->slowA.n = c->ncomp;
   for (int i = 0; i < c->ncomp * c->ncomp; ++i) c->slowA.A[i] = A[i];
   c->slow_kind = SK_LINEAR;
@@ -1185,6 +1534,7 @@ int mr_slow_none(mr_ctx* c)
 {
   if (!c) return MR_CONTRACT;
   c->slow_kind = SK_NONE;
+  c->imex = false;
   return MR_OK;
 }
 
@@ -1501,6 +1851,10 @@ int mr_step_counts(const char* text, int s_f, int m, int fast_present, int slow_
   tmp.m = m;
   tmp.fast_kind = fast_present ? FK_LINEAR : FK_NONE;
   tmp.slow_kind = slow_present ? SK_LINEAR : SK_NONE;
+  for (int i = 0; i < kMaxStages; ++i) {  // solves: one Newton iteration (linear stage problem)
+    tmp.solve_evals[i] = 2;
+    tmp.solve_nl[i] = 1;
+  }
   const Plan p = build_plan(&tmp);
   for (const Op& o : p.ops)
     if (o.type == Op::MISSING) {

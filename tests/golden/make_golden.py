@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 import oracle as O
-from paper_2211_03293_b200.configs import CONFIGS
+from paper_2211_03293_b200.configs import CONFIGS, stage_solver
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
@@ -24,13 +24,22 @@ Y0_LIN = np.array([1.0, 0.6])
 
 
 def physics_system(name, n, **kw):
-    cfg = CONFIGS[name]
+    cfg = dict(CONFIGS[name], **kw.get("override", {}))
     S, R = cfg["S"], cfg["R"]
     mech = O.mechanism(cfg["mech_seed"], S, R)
     prof = O.velocity_profiles(cfg["vel_seed"], n, n, n) if cfg["velocity"] == "random" else None
-    sysm = O.System(n, n, n, S + 1, fast=kw.get("fast", "chem"), slow="stencil", mech=mech, S=S,
-                    R=R, rho=cfg["rho"], order=cfg["order"], diffusion=cfg["diffusion"],
-                    u=cfg["u"] or (1.0, 1.0, 1.0), prof=prof)
+    imex = cfg.get("d_impl") is not None
+
+    def make(**extra):
+        return O.System(n, n, n, S + 1, fast=kw.get("fast", "chem"), slow="stencil", mech=mech,
+                        S=S, R=R, rho=cfg["rho"], order=cfg["order"], diffusion=cfg["diffusion"],
+                        u=cfg["u"] or (1.0, 1.0, 1.0), prof=prof, imex=imex,
+                        d_impl=cfg.get("d_impl") or 0.0, cg_iters=cfg.get("cg_iters") or 0,
+                        **extra)
+    sysm = make()
+    if imex:  # the ImplicitStageSolver is configured from the initial state
+        tol, safety, mx, w = stage_solver(sysm.initial_condition(cfg["ic_seed"]))
+        sysm = make(newton=(tol, safety, mx), newton_weights=w)
     return cfg, sysm
 
 
@@ -41,7 +50,9 @@ def main():
                  for n in ["mis-kw3", "imex-mri-gark4-explicit", "imex-mri-gark3b", "imex-mri-gark4"]}
 
     # 1. reacting-flow workloads on 8^3 with each config's physics and method
-    for name, steps in [("C1", 2), ("C2", 2), ("C3", 1), ("C4", 1)]:
+    # (C5: the reference's ImplicitSolve runs its own Newton-GMRES; counters
+    # n_linear_iters / n_precond_solves then describe GMRES, not the PCG)
+    for name, steps in [("C1", 2), ("C2", 2), ("C3", 1), ("C4", 1), ("C5", 1)]:
         n = 8
         cfg, sysm = physics_system(name, n)
         y0 = sysm.initial_condition(cfg["ic_seed"])
@@ -63,6 +74,19 @@ def main():
     out["transport_n12_y"] = y
     out["transport_n12_counters"] = cnt
     meta["transport_n12"] = dict(H=H, steps=3, m=4, config="C3", fast="none")
+
+    # 2b. IMEX reaction-off run: stiff enough that the implicit diffusion solve
+    #     is visible (gamma D sum 2/dx^2 ~ 0.1); one Newton iteration per solve
+    #     with the PCG converged at 8 iterations
+    over = dict(d_impl=0.05, cg_iters=8)
+    cfg, sysm = physics_system("C5", 12, fast="none", override=over)
+    y0 = sysm.initial_condition(cfg["ic_seed"])
+    H = 2e-3
+    y, cnt = sysm.mri_integrate(couplings["imex-mri-gark3b"], "kutta3", 4, 0.0, 3 * H, H, y0,
+                                use_reference=True)
+    out["imex_transport_n12_y"] = y
+    out["imex_transport_n12_counters"] = cnt
+    meta["imex_transport_n12"] = dict(H=H, steps=3, m=4, config="C5", fast="none", **over)
 
     # 3. LinearTwoRateOde per cell through the reference mri_integrate
     for cp_name, table, m in [("mis-kw3", "bogacki-shampine3", 10),
