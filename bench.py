@@ -95,10 +95,18 @@ def cpu_reference_sample(cfg_name, n_sample, steps, threads):
     n = n_sample
     mech = O.mechanism(cfg["mech_seed"], S, R)
     prof = O.velocity_profiles(cfg["vel_seed"], n, n, n) if cfg["velocity"] == "random" else None
-    sysm = O.System(n, n, n, S + 1, fast="chem", slow="stencil", mech=mech, S=S, R=R,
-                    rho=cfg["rho"], order=cfg["order"], diffusion=cfg["diffusion"],
-                    u=cfg["u"] or (1.0, 1.0, 1.0), prof=prof, threads=threads)
+
+    def make(**kw):
+        return O.System(n, n, n, S + 1, fast="chem", slow="stencil", mech=mech, S=S, R=R,
+                        rho=cfg["rho"], order=cfg["order"], diffusion=cfg["diffusion"],
+                        u=cfg["u"] or (1.0, 1.0, 1.0), prof=prof, threads=threads, **kw)
+    sysm = make()
     y = sysm.initial_condition(cfg["ic_seed"])
+    if cfg.get("d_impl") is not None:  # IMEX: f_implicit + the workload's stage solver
+        from paper_2211_03293_b200.configs import stage_solver
+        tol, safety, mx, w = stage_solver(y)
+        sysm = make(imex=True, d_impl=cfg["d_impl"], cg_iters=cfg["cg_iters"],
+                    newton=(tol, safety, mx), newton_weights=w)
     use_ref = os.path.exists(O.REF_LIB)
     cp = "mis-kw3" if cfg["coupling"] == "mis-kw3" else open(
         os.path.join(ROOT, "paper_2211_03293_b200", "data", "couplings",
@@ -168,6 +176,10 @@ def run_ours(args):
     n = args.n or cfg0["n"]
     S = cfg0["S"]
     i0, n0l = P.slab_bounds(n, world, rank)
+    if args.slab_of and world == 1:
+        # one rank's slab of a slab_of-GPU run, periodic onto itself: the
+        # per-GPU work of that run without its halo traffic
+        i0, n0l = P.slab_bounds(n, args.slab_of, 0)
     ctx = P.Context(local)
     if world > 1:
         uid = [P.Context.nccl_unique_id() if rank == 0 else None]
@@ -175,6 +187,14 @@ def run_ours(args):
         ctx.comm_init(world, rank, uid[0])
     t_setup = time.perf_counter()
     cfg, y0 = P.setup_workload(ctx, args.config, n=n, i0=i0, n0_local=n0l, threads=0)
+    if cfg.get("d_impl") is not None and dist:
+        # stage-solver weights use the GLOBAL max|y0| (configs.stage_solver)
+        import numpy as np
+        from paper_2211_03293_b200.configs import stage_solver
+        t_ = torch.tensor([float(np.abs(y0).max())], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        tol, safety, mx, w = stage_solver(y0, float(t_.item()))
+        ctx.newton_config(tol, safety, mx, w)
     setup_s = time.perf_counter() - t_setup
     H = cfg["H"]
     fp64_peak = ctx.fp64_peak()
@@ -224,14 +244,17 @@ def run_ours(args):
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     chem_ms_max = max_over_ranks(chem_ms)
     slow_ms_max = max_over_ranks(slow_ms)
-    value = float(n) ** 3 * args.steps / (ms * 1e-3)
+    ncell_job = float(n) ** 3 if world > 1 else float(ncell_local)  # cells all ranks own
+    value = ncell_job * args.steps / (ms * 1e-3)
     evals_per_cell_step = int(cnt_t[0]) // args.steps
-    chem_cells_per_s = float(n) ** 3 * evals_per_cell_step * args.steps / (chem_ms_max * 1e-3)
+    chem_cells_per_s = ncell_job * evals_per_cell_step * args.steps / (chem_ms_max * 1e-3)
     flops_per_eval = ctx.chem_flops_per_eval()
     chem_tflops = ncell_local * evals_per_cell_step * args.steps * flops_per_eval / (
         chem_ms * 1e-3) / 1e12
     slow_evals = int(cnt_t[2]) // args.steps
-    computed_slow = max(slow_evals - 1, 1)  # the final unreferenced evaluation is skipped
+    # explicit couplings: the forced final evaluation is unreferenced and only
+    # counted (mri.cpp:162-166); IMEX couplings have no forced evaluation
+    computed_slow = slow_evals if cfg.get("d_impl") is not None else max(slow_evals - 1, 1)
     stencil_bytes = 2.0 * 8 * (S + 1) * ncell_local * computed_slow * args.steps
     stencil_gbs = stencil_bytes / (slow_ms * 1e-3) / 1e9 if slow_ms > 0 else None
     pk = peaks()
@@ -258,7 +281,7 @@ def run_ours(args):
         e1.synchronize()
         barrier()
         ems = max_over_ranks(e0.elapsed_time(e1))
-        e2e = {"value": float(n) ** 3 * e_steps / (ems * 1e-3), "unit": UNIT,
+        e2e = {"value": ncell_job * e_steps / (ems * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": 8 * dof * world, "d2h_bytes_per_step": 8 * dof * world,
                "steps": e_steps, "ms_per_step": ems / e_steps}
 
@@ -275,13 +298,12 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded mechanism + initial condition)",
-            "config": {"workload": f"{args.config}: {n}^3 grid, {S} species / {cfg['R']} reactions "
-                                   f"(synthetic Arrhenius), {cfg['coupling']} (MRI-GARK-ERK45a "
-                                   f"stand-in) + {cfg['fast_table']}, H/h={cfg['m']}, "
-                                   f"order-{cfg['order']} advection-diffusion, H={H:g}",
+            "config": {"workload": workload_text(args, cfg, n, n0l, H),
                        "grid": n, "species": S, "reactions": cfg["R"],
-                       "parallelism": f"slab{world}" if world > 1 else "single GPU",
-                       "l2": "inputs > L2 (7.25 GB state)" if n >= 128 else "fits L2"},
+                       "parallelism": f"slab{world}" if world > 1 else (
+                           f"single GPU, slab 1/{args.slab_of}" if args.slab_of else "single GPU"),
+                       "l2": (f"inputs > L2 ({8 * (S + 1) * ncell_local / 1e9:.2f} GB state "
+                              f"per GPU)") if 8 * (S + 1) * ncell_local > 126e6 else "fits L2"},
             "chem_rhs_cells_per_s": chem_cells_per_s,
             "roofline": {"bound": "fp64", "kernel": "chain_kernel (fused fast IVP + chemistry)",
                          "achieved": chem_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
@@ -308,6 +330,22 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def workload_text(args, cfg, n, n0l, H):
+    if cfg.get("d_impl") is not None:
+        method = (f"{cfg['coupling']} + {cfg['fast_table']}, H/h={cfg['m']}, order-{cfg['order']} "
+                  f"advection (slow-explicit) + D={cfg['d_impl']:g} diffusion (slow-implicit, "
+                  f"Newton + {cfg['cg_iters']}-iteration Jacobi-PCG on L7)")
+    elif cfg["coupling"] == "mis-kw3":
+        method = (f"mis-kw3 (MRI-GARK-ERK33 stand-in) + {cfg['fast_table']}, H/h={cfg['m']}, "
+                  f"order-{cfg['order']} advection-diffusion")
+    else:
+        method = (f"{cfg['coupling']} (MRI-GARK-ERK45a stand-in) + {cfg['fast_table']}, "
+                  f"H/h={cfg['m']}, order-{cfg['order']} advection-diffusion")
+    grid = f"{n}^3 grid" if n0l == n else f"{n0l}x{n}x{n} slab of the {n}^3 grid"
+    return (f"{args.config}: {grid}, {cfg['S']} species / {cfg['R']} reactions (synthetic "
+            f"Arrhenius), {method}, H={H:g}")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -320,6 +358,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--slab-of", type=int, default=0,
+                    help="N=1: run one rank's slab of an N-GPU decomposition (e.g. C5: 8)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -921,7 +921,9 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
       missing_stage = o.stage;
       break;
     }
-    const int cls = o.type == Op::CHAIN ? 0 : (o.type == Op::SLOW || o.type == Op::IMPL || o.type == Op::SOLVE ? 1 : 2);
+    // profile classes: 0 fused fast IVPs, 1 explicit slow RHS (stencil),
+    // 2 everything else (updates, implicit evaluations and solves)
+    const int cls = o.type == Op::CHAIN ? 0 : (o.type == Op::SLOW ? 1 : 2);
     if (c0->profile) {
       cudaEventRecord(pool_event(c0, ev), st);
       timed.push_back({cls, ev});
