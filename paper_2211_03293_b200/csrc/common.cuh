@@ -94,6 +94,7 @@ struct ChemParams {
   // slot (w + NW*t) -> component owned by that thread; >= ncomp = idle.
   // Greedy-balanced on the species' production-list lengths.
   unsigned char perm[MR_CHEM_MAXS];
+  unsigned long long* prof;  // phase-cycle accumulators (MR_PHASE_PROF builds only)
 };
 
 struct ChemCfg {

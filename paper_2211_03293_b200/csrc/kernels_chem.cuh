@@ -122,6 +122,29 @@ __device__ __forceinline__ Smem stage(char* base, const ChemParams& P, int NW, i
   return m;
 }
 
+// Phase profiling (build with NVFLAGS_EXTRA=-DMR_PHASE_PROF): thread 0 of
+// every block accumulates clock64 deltas between the RHS phase boundaries.
+// (A clock read right after a barrier sees its issue, not its release: each
+// phase includes the wait at the barrier that opens it.)
+#ifdef MR_PHASE_PROF
+#define MR_PH(i)                                                      \
+  do {                                                                \
+    if (threadIdx.x == 0 && P.prof) {                                 \
+      const long long now_ = clock64();                               \
+      atomicAdd(&P.prof[i], (unsigned long long)(now_ - ph_last));    \
+      ph_last = now_;                                                 \
+    }                                                                 \
+  } while (0)
+#define MR_PH_ARG , long long& ph_last
+#define MR_PH_PASS , ph_last
+#else
+#define MR_PH(i) \
+  do {           \
+  } while (0)
+#define MR_PH_ARG
+#define MR_PH_PASS
+#endif
+
 template <class T>
 __device__ __forceinline__ const T& at(const char* base, unsigned off)
 {
@@ -132,8 +155,9 @@ __device__ __forceinline__ const T& at(const char* base, unsigned off)
 template <int NW, int SPL>
 __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem& m, int w, int c,
                                                 const int (&kk)[SPL], const double (&v)[SPL],
-                                                double (&f)[SPL])
+                                                double (&f)[SPL] MR_PH_ARG)
 {
+  MR_PH(0);  // RK bookkeeping since the previous evaluation
   const int S = P.S;
   const unsigned lane8 = (unsigned)c * 8u, lane16 = (unsigned)c * 16u;
   // ---- temperature from energy: partial sums of e(T) = E0 + E1 T + E2 T^2
@@ -156,6 +180,7 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
     m.part[(3 * NW + w) * 32 + c] = e;
   }
   __syncthreads();
+  MR_PH(1);  // energy partial sums
   if (w == 0) {
     double E0 = 0.0, E1 = 0.0, E2 = 0.0, ee = 0.0;
 #pragma unroll
@@ -172,6 +197,7 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
     m.tinf[2 * 32 + c] = 1.0 / T;
   }
   __syncthreads();
+  MR_PH(2);  // temperature (warp 0)
   const double T = m.tinf[0 * 32 + c];
   const double lnT = m.tinf[1 * 32 + c];
   const double invT = m.tinf[2 * 32 + c];
@@ -193,6 +219,7 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
     }
   }
   __syncthreads();
+  MR_PH(3);  // species rows
 
   double acc[SPL];
 #pragma unroll
@@ -226,6 +253,7 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
       rp += NW * (int)sizeof(ChemRec);
     }
     __syncthreads();
+    MR_PH(4);  // reactions (chunk)
     // ---- production: w_k += sum_(producing) q - sum_(consuming) q, reaction
     //      ascending, four entries per broadcast LDS.128 (padding -> zero row)
 #pragma unroll
@@ -252,6 +280,7 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
       }
     }
     if (ch + 1 < P.nchunk) __syncthreads();  // q is overwritten by the next chunk
+    MR_PH(5);  // production (warp 0's own lists)
   }
 #pragma unroll
   for (int t = 0; t < SPL; ++t) {
@@ -271,6 +300,10 @@ __global__ void __launch_bounds__(NW * 32, (NW <= 8 ? 2 : 1))  // NW*32 threads:
   const bool active = cell < a.ncell;
   const size_t nc = a.ncell;
   const int ncomp = a.ncomp;
+#ifdef MR_PHASE_PROF
+  long long ph_last = clock64();
+  const long long ph_begin = ph_last;
+#endif
   const Smem m = stage(reinterpret_cast<char*>(smem_raw), P, NW, c, w);
   int kk[SPL];  // components owned by this thread (load-balanced permutation)
 #pragma unroll
@@ -369,7 +402,7 @@ __global__ void __launch_bounds__(NW * 32, (NW <= 8 ? 2 : 1))  // NW*32 threads:
         const double theta = dadd(t0, dmul(a.tab.c[j], h));
         const double tau = __ddiv_rn(dadd(theta, -st.t_start), st.span);
         double f[SPL];
-        chem_block_eval<NW, SPL>(P, m, w, c, kk, stg, f);
+        chem_block_eval<NW, SPL>(P, m, w, c, kk, stg, f MR_PH_PASS);
         const double hb = dmul(h, a.tab.b[j]);
         const bool use_b = a.tab.b[j] != 0.0;
         double hA_next = 0.0;
@@ -419,6 +452,12 @@ __global__ void __launch_bounds__(NW * 32, (NW <= 8 ? 2 : 1))  // NW*32 threads:
     const int k = kk[t];
     if (active && k < ncomp) a.y_out[(size_t)k * nc + cell] = y[t];
   }
+#ifdef MR_PHASE_PROF
+  if (threadIdx.x == 0 && P.prof) {
+    atomicAdd(&P.prof[6], (unsigned long long)(clock64() - ph_begin));
+    atomicAdd(&P.prof[7], 1ull);
+  }
+#endif
 }
 
 template <int NW, int SPL>
@@ -442,7 +481,10 @@ __global__ void __launch_bounds__(NW * 32) chem_rhs_kernel(const double* __restr
     const int k = kk[t];
     v[t] = (active && k < ncomp) ? yin[(size_t)k * nc + cell] : 0.0;
   }
-  chem_block_eval<NW, SPL>(P, m, w, c, kk, v, f);
+#ifdef MR_PHASE_PROF
+  long long ph_last = clock64();
+#endif
+  chem_block_eval<NW, SPL>(P, m, w, c, kk, v, f MR_PH_PASS);
 #pragma unroll
   for (int t = 0; t < SPL; ++t) {
     const int k = kk[t];

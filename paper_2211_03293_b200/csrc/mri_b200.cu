@@ -1318,6 +1318,15 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
   P.S = S;
   P.R = R;
   P.RuP = kRu / kPatm;
+#ifdef MR_PHASE_PROF
+  {
+    unsigned long long* pp = nullptr;
+    MR_CUDA_TRY(c, cudaMalloc(&pp, 8 * sizeof(unsigned long long)));
+    MR_CUDA_TRY(c, cudaMemset(pp, 0, 8 * sizeof(unsigned long long)));
+    c->chem_bufs.push_back(pp);
+    P.prof = pp;
+  }
+#endif
   for (int k = 0; k < S; ++k) {
     P.h0[k] = sp[0 * Sp + k]; P.a[k] = sp[1 * Sp + k]; P.hb[k] = sp[2 * Sp + k];
     P.s0[k] = sp[3 * Sp + k]; P.rhoW[k] = sp[4 * Sp + k]; P.Wrho[k] = sp[5 * Sp + k];
@@ -1868,6 +1877,19 @@ int mr_step_counts(const char* text, int s_f, int m, int fast_present, int slow_
 }
 
 // ---------------- instrumentation ----------------
+// Debug (not part of include/mri_b200.h): chemistry phase cycles of an
+// MR_PHASE_PROF build, summed over blocks; out[7] = blocks.  reset zeroes them.
+int mr_debug_chem_phases(mr_ctx* c, uint64_t* out, int reset)
+{
+  if (!c || !c->chemP || !c->chemP->prof) return MR_CONTRACT;
+  cudaSetDevice(c->device);
+  MR_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (out)
+    MR_CUDA_TRY(c, cudaMemcpy(out, c->chemP->prof, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  if (reset) MR_CUDA_TRY(c, cudaMemset(c->chemP->prof, 0, 8 * sizeof(uint64_t)));
+  return MR_OK;
+}
+
 void* mr_stream(mr_ctx* c) { return c ? (void*)c->stream : nullptr; }
 uint64_t mr_launch_count(const mr_ctx* c) { return c ? c->launches : 0; }
 double mr_chem_flops_per_eval(const mr_ctx* c) { return c ? c->chem_flops : 0.0; }
