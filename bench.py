@@ -85,6 +85,19 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of the dominant kernels from the committed
+    ncu --set full captures (profiles/<latest round>/traffic.json)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")))
+    if not files:
+        return {}
+    try:
+        return json.load(open(files[-1]))
+    except (OSError, ValueError):
+        return {}
+
+
 def cpu_reference_sample(cfg_name, n_sample, steps, threads):
     """Time the reference's own mri_step (oracle/_ref) with the CPU physics on
     an n_sample^3 sub-grid of the workload (same mechanism, method, m, stencil)."""
@@ -258,6 +271,7 @@ def run_ours(args):
     stencil_bytes = 2.0 * 8 * (S + 1) * ncell_local * computed_slow * args.steps
     stencil_gbs = stencil_bytes / (slow_ms * 1e-3) / 1e9 if slow_ms > 0 else None
     pk = peaks()
+    tr = ncu_traffic()
     ctx.set_profiling(False)
 
     # ---------------- end-to-end through the host-buffer C-ABI ----------------
@@ -308,13 +322,20 @@ def run_ours(args):
             "roofline": {"bound": "fp64", "kernel": "chain_kernel (fused fast IVP + chemistry)",
                          "achieved": chem_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": chem_tflops / fp64_peak if fp64_peak else None,
-                         "traffic": None,
+                         "traffic": tr.get("chem_chain", {}).get("dram_bytes_per_launch"),
+                         "traffic_algorithmic": tr.get("chem_chain", {}).get(
+                             "algorithmic_bytes_per_launch"),
+                         "traffic_source": tr.get("chem_chain", {}).get("source"),
                          "flops_per_eval": flops_per_eval,
                          "peak_source": "DFMA-chain microbenchmark in this run (MEASURED_PEAKS.json "
                                         "has no fp64 figure)"},
             "roofline_stencil": {"bound": "hbm", "achieved": stencil_gbs,
                                  "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                                  "frac": (stencil_gbs / pk["hbm_gbs"]) if stencil_gbs else None,
+                                 "traffic": tr.get("stencil", {}).get("dram_bytes_per_launch"),
+                                 "traffic_algorithmic": tr.get("stencil", {}).get(
+                                     "algorithmic_bytes_per_launch"),
+                                 "traffic_source": tr.get("stencil", {}).get("source"),
                                  "bytes_per_eval": 16.0 * (S + 1) * ncell_local},
             "time_split_ms": {"chem": chem_ms_max, "slow": slow_ms_max, "other": other_ms},
             "e2e": e2e,

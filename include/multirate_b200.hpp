@@ -7,7 +7,8 @@
 //   Mode B (device-resident step, the product path):
 //     multirate::b200::Device dev(0);
 //     dev.grid(n, n, n, S + 1);  dev.chemistry(...);  dev.stencil(...);
-//     y = multirate::b200::mri_integrate(dev, method, t0, tf, H, y0, counters);
+//     [dev.implicit_diffusion(d, cg_iters);   // IMEX couplings]
+//     y = multirate::b200::mri_integrate(dev, method, [solver,] t0, tf, H, y0, counters);
 //   Mode A (the reference's own mri_step driving GPU callbacks):
 //     PartitionedSystem sys = multirate::b200::partitioned_system(dev);
 //     y = multirate::mri_integrate(method, sys, solver, t0, tf, H, y0, counters);
@@ -58,17 +59,43 @@ public:
                  const int* rspecies)
   {
     check(mr_fast_chemistry(ctx_, S, R, rho, species, reactions, rspecies));
+    fast_ = true;
+  }
+  void no_fast()  // f_fast absent
+  {
+    check(mr_fast_none(ctx_));
+    fast_ = false;
   }
   void stencil(int order, double diffusion, const double* u, const double* prof = nullptr,
                int nmax = 0)
   {
     check(mr_slow_stencil(ctx_, order, diffusion, u, prof, nmax));
+    imex_ = false;
+  }
+  // IMEX split of the slow partition (after stencil): f_implicit = d_impl L7
+  void implicit_diffusion(double d_impl, int cg_iters)
+  {
+    check(mr_slow_implicit_diffusion(ctx_, d_impl, cg_iters));
+    imex_ = true;
+  }
+  // ImplicitStageSolver (mri.hpp:71-78): NewtonConfig + WRMS weights.  The
+  // GMRES settings and make_preconditioner do not apply: the device solves
+  // the linear stage problem with its fixed-iteration PCG.
+  void solver(const ImplicitStageSolver& s)
+  {
+    const bool w = s.weights.size() == dof_ && dof_ > 0;
+    check(mr_newton_config(ctx_, s.newton.tolerance, s.newton.safety, s.newton.max_iters,
+                           w ? s.weights.data() : nullptr));
   }
   std::size_t dof() const { return dof_; }
+  bool imex() const { return imex_; }
+  bool has_fast() const { return fast_; }
 
 private:
   mr_ctx* ctx_ = nullptr;
   std::size_t dof_ = 0;
+  bool imex_ = false;
+  bool fast_ = false;
 };
 
 inline void to_c(const EvalCounters& c, uint64_t* o)
@@ -128,6 +155,14 @@ inline StateVector mri_step(Device& d, const MriMethodConfig& mc, double t, cons
   return out;
 }
 
+// mri_step with the reference's ImplicitStageSolver (IMEX couplings)
+inline StateVector mri_step(Device& d, const MriMethodConfig& mc, const ImplicitStageSolver& solver,
+                            double t, const StateVector& y, double H, EvalCounters& counters)
+{
+  d.solver(solver);
+  return mri_step(d, mc, t, y, H, counters);
+}
+
 // mri_integrate (mri.hpp:129-133): the state stays in HBM between steps.
 inline StateVector mri_integrate(Device& d, const MriMethodConfig& mc, double t0, double tf,
                                  double H, const StateVector& y0, EvalCounters& counters)
@@ -146,6 +181,15 @@ inline StateVector mri_integrate(Device& d, const MriMethodConfig& mc, double t0
   return out;
 }
 
+// mri_integrate with the reference's ImplicitStageSolver (IMEX couplings)
+inline StateVector mri_integrate(Device& d, const MriMethodConfig& mc,
+                                 const ImplicitStageSolver& solver, double t0, double tf,
+                                 double H, const StateVector& y0, EvalCounters& counters)
+{
+  d.solver(solver);
+  return mri_integrate(d, mc, t0, tf, H, y0, counters);
+}
+
 // "Mode A": the reference's PartitionedSystem (partitioned_system.hpp:25-61)
 // whose f_fast / f_explicit callbacks evaluate the device plugins.
 inline PartitionedSystem partitioned_system(Device& d)
@@ -153,16 +197,30 @@ inline PartitionedSystem partitioned_system(Device& d)
   PartitionedSystem sys;
   sys.dimension = d.dof();
   Device* dp = &d;
-  sys.f_fast = [dp](double t, const StateVector& y) {
-    StateVector out(y.size());
-    dp->check(mr_fast_rhs(dp->ctx(), t, y.data(), out.data()));
-    return out;
-  };
+  if (d.has_fast())
+    sys.f_fast = [dp](double t, const StateVector& y) {
+      StateVector out(y.size());
+      dp->check(mr_fast_rhs(dp->ctx(), t, y.data(), out.data()));
+      return out;
+    };
   sys.f_explicit = [dp](double t, const StateVector& y) {
     StateVector out(y.size());
     dp->check(mr_slow_rhs(dp->ctx(), t, y.data(), out.data()));
     return out;
   };
+  if (d.imex()) {
+    sys.f_implicit = [dp](double t, const StateVector& y) {
+      StateVector out(y.size());
+      dp->check(mr_implicit_rhs(dp->ctx(), t, y.data(), out.data()));
+      return out;
+    };
+    // f_implicit is linear: J v = f_implicit(v)
+    sys.jv_implicit = [dp](double t, const StateVector&, const StateVector& v) {
+      StateVector out(v.size());
+      dp->check(mr_implicit_rhs(dp->ctx(), t, v.data(), out.data()));
+      return out;
+    };
+  }
   return sys;
 }
 

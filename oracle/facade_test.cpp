@@ -39,11 +39,17 @@ double rel_err(const StateVector& a, const StateVector& b, int ncomp)
 }
 }  // namespace
 
+// d_impl >= 0 selects the IMEX split (explicit stencil diffusion `diffusion`,
+// implicit d_impl L7 with cg_iters PCG iterations on the device); newton =
+// {tolerance, safety, max_iters} and weights (may be NULL) configure the
+// ImplicitStageSolver used by all three paths.
 extern "C" int facade_selftest(int n, int S, int R, double rho, const double* species,
                                const double* reactions, const int* rspecies, const double* y0in,
                                const char* coupling, const char* table, int m, int order,
-                               double H, int steps, double* errs, uint64_t* counters, char* err,
-                               size_t errlen)
+                               double H, int steps, int fast, double diffusion, double d_impl,
+                               int cg_iters,
+                               const double* newton, const double* weights, double* errs,
+                               uint64_t* counters, char* err, size_t errlen)
 {
   try {
     const int ncomp = S + 1;
@@ -61,15 +67,35 @@ extern "C" int facade_selftest(int n, int S, int R, double rho, const double* sp
     mc.m = m;
     const double u[3] = {1.0, 1.0, 1.0};
 
+    const bool imex = d_impl >= 0.0;
+    ImplicitStageSolver solver;
+    if (newton) {
+      solver.newton.tolerance = newton[0];
+      solver.newton.safety = newton[1];
+      solver.newton.max_iters = (int)newton[2];
+    }
+    if (weights) {
+      solver.weights = StateVector(dof);
+      std::memcpy(solver.weights.data(), weights, dof * sizeof(double));
+    }
+    // the reference's GMRES only has to converge (the device uses its PCG)
+    double ymax = 0.0;
+    for (double v : y0) ymax = std::max(ymax, std::fabs(v));
+    solver.gmres.tolerance = 1e-15 * (1.0 + ymax);
+    solver.gmres.safety = 1.0;
+    solver.gmres.max_iters = 200;
+
     b200::Device dev(0);
     dev.grid(n, n, n, ncomp);
     dev.chemistry(S, R, rho, species, reactions, rspecies);
-    dev.stencil(order, 1e-3, u);
+    if (!fast) dev.no_fast();
+    dev.stencil(order, diffusion, u);
+    if (imex) dev.implicit_diffusion(d_impl, cg_iters);
 
     EvalCounters cB, cA, cC;
-    StateVector yB = b200::mri_integrate(dev, mc, 0.0, steps * H, H, y0, cB);
+    StateVector yB = b200::mri_integrate(dev, mc, solver, 0.0, steps * H, H, y0, cB);
     PartitionedSystem sysA = b200::partitioned_system(dev);
-    StateVector yA = mri_integrate(mc, sysA, ImplicitStageSolver{}, 0.0, steps * H, H, y0, cA);
+    StateVector yA = mri_integrate(mc, sysA, solver, 0.0, steps * H, H, y0, cA);
 
     orc_sys_cfg cfg;
     std::memset(&cfg, 0, sizeof(cfg));
@@ -77,27 +103,43 @@ extern "C" int facade_selftest(int n, int S, int R, double rho, const double* sp
     cfg.n0_global = n;
     cfg.ncomp = ncomp;
     cfg.length = 1.0;
-    cfg.fast_kind = ORC_FAST_CHEM;
+    cfg.fast_kind = fast ? ORC_FAST_CHEM : ORC_FAST_NONE;
     cfg.slow_kind = ORC_SLOW_STENCIL;
     cfg.S = S; cfg.R = R; cfg.rho = rho;
     cfg.species = species; cfg.reactions = reactions; cfg.rspecies = rspecies;
-    cfg.order = order; cfg.diffusion = 1e-3; cfg.vel_kind = 0;
+    cfg.order = order; cfg.diffusion = diffusion; cfg.vel_kind = 0;
     cfg.u_const[0] = cfg.u_const[1] = cfg.u_const[2] = 1.0;
     cfg.threads = 1;
+    cfg.imex = imex ? 1 : 0;
+    cfg.d_impl = imex ? d_impl : 0.0;
+    cfg.cg_iters = cg_iters;
     orc_sys* cs = orc_sys_create(&cfg);
     PartitionedSystem sysC;
     sysC.dimension = dof;
-    sysC.f_fast = [cs](double t, const StateVector& y) {
-      StateVector o(y.size());
-      orc_sys_fast_rhs(cs, t, y.data(), o.data());
-      return o;
-    };
+    if (fast)
+      sysC.f_fast = [cs](double t, const StateVector& y) {
+        StateVector o(y.size());
+        orc_sys_fast_rhs(cs, t, y.data(), o.data());
+        return o;
+      };
     sysC.f_explicit = [cs](double t, const StateVector& y) {
       StateVector o(y.size());
       orc_sys_slow_rhs(cs, t, y.data(), o.data());
       return o;
     };
-    StateVector yC = mri_integrate(mc, sysC, ImplicitStageSolver{}, 0.0, steps * H, H, y0, cC);
+    if (imex) {
+      sysC.f_implicit = [cs](double t, const StateVector& y) {
+        StateVector o(y.size());
+        orc_sys_implicit_rhs(cs, t, y.data(), o.data());
+        return o;
+      };
+      sysC.jv_implicit = [cs](double t, const StateVector&, const StateVector& v) {
+        StateVector o(v.size());
+        orc_sys_implicit_rhs(cs, t, v.data(), o.data());
+        return o;
+      };
+    }
+    StateVector yC = mri_integrate(mc, sysC, solver, 0.0, steps * H, H, y0, cC);
     orc_sys_destroy(cs);
 
     errs[0] = rel_err(yB, yC, ncomp);
