@@ -74,7 +74,7 @@ struct ChemDev {
 struct ChemRec {           // 48 B, one per reaction
   double lnA, beta, EaR;
   unsigned r1o, r2o;       // byte offsets of the reactant rows in the (C, E') double2 table
-  unsigned p1o, p2o;       // byte offsets of the product rows in the D' table
+  unsigned p1o, p2o;       // byte offsets of the product rows in the D' table (absent: dummy row)
   unsigned pad0, pad1;
 };
 struct ChemParams {

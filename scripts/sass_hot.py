@@ -35,3 +35,29 @@ order = sorted(range(len(data)), key=lambda k: -data[k][2])[:N]
 for k in sorted(order):
     a, src, s, i = data[k]
     print(f"{k:5d} {100 * s / tot_s:5.2f}% {i:>12d}  {src[:90]}")
+
+# stall reasons: total, and per code region given as "lo:hi" instruction-index ranges (argv[3:])
+reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+ridx = [ix[h] for h in reasons]
+rows2 = [r for r in rows[2:] if len(r) >= len(hdr)]
+
+
+def region(lo, hi):
+    tot = [0] * len(reasons)
+    for r in rows2[lo:hi]:
+        for q, i in enumerate(ridx):
+            try:
+                tot[q] += int(r[i] or 0)
+            except ValueError:
+                pass
+    return tot
+
+
+specs = sys.argv[3:] or ["0:%d" % len(rows2)]
+for sp in specs:
+    lo, hi = (int(x) for x in sp.split(":"))
+    tot = region(lo, hi)
+    ssum = sum(tot) or 1
+    top = sorted(zip(reasons, tot), key=lambda t: -t[1])[:8]
+    print(f"\nstall reasons [{lo}:{hi}] ({ssum} samples, {100 * ssum / tot_s:.1f}% of all):")
+    print("  " + ", ".join(f"{n[6:]} {100 * v / ssum:.0f}%" for n, v in top))
