@@ -305,8 +305,16 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
   }
 }
 
+// Resident blocks per SM requested from ptxas (register budget), measured per
+// layout on C1-C3 (one B200): NW = 4 -> 8 blocks for degree-1 forcing (C1:
+// 0.48 -> 0.39 ms/step), 6 for degree 2 (C2: 5.42 -> 4.69); NW = 8 -> 4 (C3:
+// 229 -> 196); NW = 32 is one 1024-thread block (64 registers).
+constexpr int chem_min_blocks(int NW, int NDEG)
+{
+  return NW == 4 ? (NDEG == 1 ? 8 : 6) : NW == 8 ? 4 : NW <= 16 ? 2 : 1;
+}
 template <int NW, int SPL, bool SUBDIAG, int MAXS, int NDEG>
-__global__ void __launch_bounds__(NW * 32, (NW <= 8 ? 2 : 1))  // NW*32 threads: 1024 -> 64 regs
+__global__ void __launch_bounds__(NW * 32, chem_min_blocks(NW, NDEG))
     chem_chain_kernel(const __grid_constant__ ChainArgs a, const __grid_constant__ ChemParams P)
 {
   extern __shared__ __align__(16) double smem_raw[];
