@@ -142,6 +142,13 @@ int mr_mri_integrate(mr_ctx* ctx, double t0, double tf, double H, uint64_t* coun
 /* End-to-end variant with HOST buffers: H2D of y_in, the step, D2H of y_out. */
 int mr_mri_step_host(mr_ctx* ctx, double t, double H, const double* y_in, double* y_out,
                      uint64_t* counters, int* fail_stage);
+/* reference_solution (proj/src/erk.cpp:59-75): single-rate cash-karp5
+ * (erk_integrate, :40-57) of the summed right-hand side f_fast + f_implicit +
+ * f_explicit (partitioned_system.hpp:41-48) from t0 to tf with step h_ref, on
+ * the device-resident state (the reference solution of the convergence /
+ * efficiency studies, harness.cpp:411-429).  No counters.  On MR_INTEGRATION
+ * the state is unchanged and *fail_stage is erk_step's stage index. */
+int mr_reference_solution(mr_ctx* ctx, double t0, double tf, double h_ref, int* fail_stage);
 /* Location of the last failure: MRI stage, fast substep, inner stage. */
 int mr_last_failure(const mr_ctx* ctx, int* mri_stage, int* substep, int* inner_stage);
 

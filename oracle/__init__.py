@@ -102,6 +102,8 @@ def lib():
         for fn in ("orc_sys_mri_step",):
             getattr(L, fn).argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int, C.c_double,
                                        C.c_double, _dp, _u64p, _ip, C.c_char_p, C.c_size_t]
+        L.orc_sys_reference_solution.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double,
+                                                 _dp, _ip, C.c_char_p, C.c_size_t]
         L.orc_sys_mri_integrate.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int,
                                             C.c_double, C.c_double, C.c_double, _dp, _u64p, _ip,
                                             C.c_char_p, C.c_size_t]
@@ -136,6 +138,8 @@ def ref():
         L.ref_coupling_info.argtypes = [C.c_char_p, C.c_int, _ip, _ip, _ip, _ip, _dp]
         L.ref_sys_mri_step.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int, C.c_double,
                                        C.c_double, _dp, _u64p, _ip, C.c_char_p, C.c_size_t]
+        L.ref_sys_reference_solution.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double,
+                                                 _dp, _ip, C.c_char_p, C.c_size_t]
         L.ref_sys_mri_integrate.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int,
                                             C.c_double, C.c_double, C.c_double, _dp, _u64p, _ip,
                                             C.c_char_p, C.c_size_t]
@@ -295,6 +299,18 @@ class System:
         if rc:
             raise StepError(rc, stage, err, cnt)
         return y2, cnt
+
+
+    def reference_solution(self, t0, tf, h_ref, y, use_reference=False):
+        """reference_solution (erk.cpp:59-75): cash-karp5 on the summed RHS."""
+        fn = ref().ref_sys_reference_solution if use_reference else lib().orc_sys_reference_solution
+        y2 = np.array(y, dtype=np.float64, copy=True)
+        stage = C.c_int(-1)
+        err = C.create_string_buffer(512)
+        rc = fn(self.h, t0, tf, h_ref, _ptr(y2), C.byref(stage), err, 512)
+        if rc:
+            raise StepError(rc, stage.value, err.value.decode())
+        return y2
 
 
 def export_coupling(name: str) -> str:

@@ -151,6 +151,18 @@ int orc_table_lookup(const char* name, orc_table* t)
     t->A[1][0] = 0.5; t->A[2][1] = 0.5; t->A[3][2] = 1;
     t->b[0] = 1.0 / 6.0; t->b[1] = 1.0 / 3.0; t->b[2] = 1.0 / 3.0; t->b[3] = 1.0 / 6.0;
     t->c[1] = 0.5; t->c[2] = 0.5; t->c[3] = 1;
+  } else if (!strcmp(name, "cash-karp5")) { /* butcher.cpp:305-321 */
+    table_zero(t, 6, 5);
+    t->A[1][0] = 1.0 / 5.0;
+    t->A[2][0] = 3.0 / 40.0; t->A[2][1] = 9.0 / 40.0;
+    t->A[3][0] = 3.0 / 10.0; t->A[3][1] = -9.0 / 10.0; t->A[3][2] = 6.0 / 5.0;
+    t->A[4][0] = -11.0 / 54.0; t->A[4][1] = 5.0 / 2.0; t->A[4][2] = -70.0 / 27.0;
+    t->A[4][3] = 35.0 / 27.0;
+    t->A[5][0] = 1631.0 / 55296.0; t->A[5][1] = 175.0 / 512.0; t->A[5][2] = 575.0 / 13824.0;
+    t->A[5][3] = 44275.0 / 110592.0; t->A[5][4] = 253.0 / 4096.0;
+    t->b[0] = 37.0 / 378.0; t->b[2] = 250.0 / 621.0; t->b[3] = 125.0 / 594.0;
+    t->b[5] = 512.0 / 1771.0;
+    t->c[1] = 1.0 / 5.0; t->c[2] = 3.0 / 10.0; t->c[3] = 3.0 / 5.0; t->c[4] = 1; t->c[5] = 7.0 / 8.0;
   } else if (!strcmp(name, "knoth-wolke3")) { /* butcher.cpp:347-362 */
     table_zero(t, 3, 3);
     t->A[1][0] = 1.0 / 3.0; t->A[2][0] = -3.0 / 16.0; t->A[2][1] = 15.0 / 16.0;
@@ -1151,6 +1163,81 @@ int orc_mri_integrate(const orc_coupling* cp, const orc_table* fast, int m, cons
   return rc;
 }
 
+/* PartitionedSystem::sum_rhs, proj/include/multirate/partitioned_system.hpp:41-48:
+ * out = 0; out += 1.0 f_fast; out += 1.0 f_implicit; out += 1.0 f_explicit */
+static void sum_rhs(const orc_problem* p, double t, const double* y, double* out, double* tmp)
+{
+  const size_t dof = p->ncell * (size_t)p->ncomp;
+  memset(out, 0, sizeof(double) * dof);
+  if (p->fast_kind != ORC_FAST_NONE) {
+    orc_fast_rhs(p, t, y, tmp);
+    axpy_into(out, 1.0, tmp, dof);
+  }
+  if (p->slow_kind == ORC_SLOW_STENCIL && p->grid && p->grid->imex) {
+    orc_implicit_rhs(p, t, y, tmp);
+    axpy_into(out, 1.0, tmp, dof);
+  }
+  if (p->slow_kind != ORC_SLOW_NONE) {
+    orc_slow_rhs(p, t, y, tmp);
+    axpy_into(out, 1.0, tmp, dof);
+  }
+}
+
+/* reference_solution, proj/src/erk.cpp:59-75: erk_integrate (:40-57) of the
+ * registered cash-karp5 table (butcher.cpp:305-321) on sum_rhs; erk_step
+ * (:9-38) semantics, no counters.  y is overwritten on success. */
+int orc_reference_solution(const orc_problem* p, double t0, double tf, double h, double* y,
+                           int* fail_stage, char* err, size_t errlen)
+{
+  *fail_stage = -1;
+  if (tf <= t0) { if (err) snprintf(err, errlen, "erk_integrate: tf must exceed t0"); return ORC_CONTRACT; }
+  if (h <= 0.0) { if (err) snprintf(err, errlen, "erk_integrate: h must be positive"); return ORC_CONTRACT; }
+  orc_table tb;
+  if (orc_table_lookup("cash-karp5", &tb) != ORC_OK) return ORC_CONTRACT;
+  const size_t dof = p->ncell * (size_t)p->ncomp;
+  const int s = tb.s;
+  double* k[ORC_MAX_TABLE];
+  for (int i = 0; i < s; ++i) k[i] = (double*)malloc(sizeof(double) * dof);
+  double* stage = (double*)malloc(sizeof(double) * dof);
+  double* tmp = (double*)malloc(sizeof(double) * dof);
+  double* work = (double*)malloc(sizeof(double) * dof);
+  memcpy(work, y, sizeof(double) * dof);
+  const long n_steps = (long)ceil((tf - t0) / h - 1e-12);
+  double t = t0;
+  int rc = ORC_OK;
+  for (long n = 0; n < n_steps && rc == ORC_OK; ++n) {
+    const double step = (n == n_steps - 1) ? (tf - t) : h;
+    for (int i = 0; i < s && rc == ORC_OK; ++i) {
+      memcpy(stage, work, sizeof(double) * dof);
+      for (int j = 0; j < i; ++j)
+        if (tb.A[i][j] != 0.0) axpy_into(stage, step * tb.A[i][j], k[j], dof);
+      if (!orc_all_finite(stage, dof)) {
+        if (err) snprintf(err, errlen, "erk_step: non-finite stage value");
+        *fail_stage = i;
+        rc = ORC_INTEGRATION;
+        break;
+      }
+      sum_rhs(p, t + tb.c[i] * step, stage, k[i], tmp);
+    }
+    if (rc != ORC_OK) break;
+    memcpy(stage, work, sizeof(double) * dof);
+    for (int i = 0; i < s; ++i)
+      if (tb.b[i] != 0.0) axpy_into(stage, step * tb.b[i], k[i], dof);
+    if (!orc_all_finite(stage, dof)) {
+      if (err) snprintf(err, errlen, "erk_step: non-finite result");
+      *fail_stage = s;
+      rc = ORC_INTEGRATION;
+      break;
+    }
+    memcpy(work, stage, sizeof(double) * dof);
+    t = (n == n_steps - 1) ? tf : t0 + (double)(n + 1) * h;
+  }
+  if (rc == ORC_OK) memcpy(y, work, sizeof(double) * dof);
+  for (int i = 0; i < s; ++i) free(k[i]);
+  free(stage); free(tmp); free(work);
+  return rc;
+}
+
 /* ------------------------------------------------------------------ */
 /* Flat session API for ctypes callers (tests, bench cpu_baseline)     */
 /* ------------------------------------------------------------------ */
@@ -1287,4 +1374,10 @@ int orc_sys_mri_integrate(orc_sys* s, const char* coupling, const char* fast_tab
   rc = orc_mri_integrate(&cp, &tb, m, &s->prob, t0, tf, H, y, &c, fail_stage, err, errlen);
   counters_out(&c, counters);
   return rc;
+}
+
+int orc_sys_reference_solution(orc_sys* s, double t0, double tf, double h, double* y,
+                               int* fail_stage, char* err, size_t errlen)
+{
+  return orc_reference_solution(&s->prob, t0, tf, h, y, fail_stage, err, errlen);
 }

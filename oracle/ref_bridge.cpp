@@ -269,3 +269,16 @@ int ref_erk_step_linear(const char* table, int n, const double* A, double t, dou
 }
 
 } // extern "C"
+
+// multirate::reference_solution (erk.cpp:59-75) on the oracle physics
+extern "C" int ref_sys_reference_solution(orc_sys* sys, double t0, double tf, double h, double* y,
+                                          int* fail_stage, char* err, size_t errlen)
+{
+  return guarded(err, errlen, fail_stage, [&] {
+    PartitionedSystem ps = make_system(sys);
+    StateVector yv(ps.dimension);
+    std::memcpy(yv.data(), y, sizeof(double) * ps.dimension);
+    StateVector out = reference_solution(ps, yv, t0, tf, h);
+    std::memcpy(y, out.data(), sizeof(double) * ps.dimension);
+  });
+}

@@ -94,6 +94,7 @@ def lib():
         "mr_slow_implicit_diffusion": (C.c_int, [vp, C.c_double, C.c_int]),
         "mr_implicit_rhs": (C.c_int, [vp, C.c_double, _dp, _dp]),
         "mr_newton_config": (C.c_int, [vp, C.c_double, C.c_double, C.c_int, _dp]),
+        "mr_reference_solution": (C.c_int, [vp, C.c_double, C.c_double, C.c_double, _ip]),
         "mr_state_upload": (C.c_int, [vp, _dp]),
         "mr_state_download": (C.c_int, [vp, _dp]),
         "mr_state_device_ptr": (C.c_void_p, [vp]),
@@ -371,6 +372,13 @@ class Context:
                                      C.byref(stage))
         self._check(rc, stage.value)
         return cnt
+
+    def reference_solution(self, t0, tf, h_ref):
+        """reference_solution (erk.cpp:59-75): cash-karp5 on f_fast + f_implicit +
+        f_explicit, applied to the device-resident state."""
+        stage = C.c_int(-1)
+        rc = self.L.mr_reference_solution(self.h, t0, tf, h_ref, C.byref(stage))
+        self._check(rc, stage.value)
 
     def last_failure(self):
         a, b, c = C.c_int(), C.c_int(), C.c_int()

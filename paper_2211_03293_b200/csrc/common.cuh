@@ -196,6 +196,8 @@ cudaError_t launch_part_sum(const double* part, double* sc, int slot, cudaStream
 cudaError_t launch_scalar_combine(double* const* scs, int n, int slot, cudaStream_t st);
 cudaError_t launch_gathered_sum(const double* g, int n, double* sc, int slot, cudaStream_t st);
 cudaError_t launch_scalar_copy(double* sc, int dst, int src, cudaStream_t st);
+cudaError_t launch_sum_rhs(size_t n, const double* ff, const double* fi, const double* fe,
+                           double* out, cudaStream_t st);
 cudaError_t launch_recover_fi(size_t n, double gamma, const double* Y, const double* known,
                               double* fI, int mri_stage, unsigned long long* fail,
                               cudaStream_t st);

@@ -630,6 +630,21 @@ __global__ void __launch_bounds__(256) recover_fi_kernel(size_t n, double gamma,
 
 }  // namespace
 
+// PartitionedSystem::sum_rhs (partitioned_system.hpp:41-48): out = 0;
+// out += 1.0 f_fast; out += 1.0 f_implicit; out += 1.0 f_explicit (absent: null)
+static __global__ void __launch_bounds__(256) sum_rhs_kernel(size_t n, const double* ff, const double* fi,
+                                                      const double* fe, double* out)
+{
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    double o = 0.0;
+    if (ff) o = __dadd_rn(o, __dmul_rn(1.0, ff[i]));
+    if (fi) o = __dadd_rn(o, __dmul_rn(1.0, fi[i]));
+    if (fe) o = __dadd_rn(o, __dmul_rn(1.0, fe[i]));
+    out[i] = o;
+  }
+}
+
 int lap_blocks() { return kLapBlocks; }
 
 cudaError_t launch_lap7(int mode, const LapArgs& a, const double* y, const double* lo,
@@ -682,6 +697,16 @@ cudaError_t launch_gathered_sum(const double* g, int n, double* sc, int slot, cu
 cudaError_t launch_scalar_copy(double* sc, int dst, int src, cudaStream_t st)
 {
   scalar_copy_kernel<<<1, 1, 0, st>>>(sc, dst, src);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_rhs(size_t n, const double* ff, const double* fi, const double* fe,
+                           double* out, cudaStream_t st)
+{
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks == 0) blocks = 1;
+  sum_rhs_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, ff, fi, fe, out);
   return cudaGetLastError();
 }
 

@@ -189,6 +189,7 @@ struct mr_ctx {
   double* cg_sc = nullptr;      // [0] rz, [1] pAp, [2] rz_new, [3] sum (G w)^2
   double* cg_gather = nullptr;  // [nranks] for the cross-rank fixed-order sum
   double* newton_w = nullptr;   // ImplicitStageSolver::weights (local slab); null = unit
+  std::vector<double*> rs_bufs;  // reference solution: k[6], stage, f_fast, f_implicit
   double newton_tol = 1.0e-10;  // NewtonConfig defaults (solvers.hpp:19-23)
   double newton_safety = 0.1;
   int newton_max = 10;
@@ -273,6 +274,8 @@ void free_state(mr_ctx* c)
   free_dev_t(c->cg_p);
   free_dev_t(c->cg_q);
   free_dev_t(c->newton_w);  // weights are per grid
+  for (auto& p : c->rs_bufs) free_dev_t(p);
+  c->rs_bufs.clear();
   c->halo_elems = 0;
   c->state_valid = false;
 }
@@ -1687,6 +1690,137 @@ int mr_fast_rhs(mr_ctx* c, double t, const double* y, double* out)
   MR_CUDA_TRY(c, cudaMemcpyAsync(out, c->scr_out, c->dof * sizeof(double), cudaMemcpyDeviceToHost,
                                  c->stream));
   MR_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MR_OK;
+}
+
+// one fast-partition RHS evaluation between device buffers
+static int eval_fast_dev(mr_ctx* c, const double* in, double* out)
+{
+  if (c->fast_kind == FK_CHEM) {
+    ChemCfg ccfg;
+    TableDev t4{};
+    t4.s = 4;
+    if (chem_pick(&ccfg, c->ncomp, c->S, c->R, t4, 1))
+      return set_err(c, MR_CONTRACT, "unsupported mechanism size");
+    MR_CUDA_TRY(c, launch_chem_rhs(ccfg, in, out, c->ncell, c->ncomp, *c->chemP, c->stream));
+  } else {
+    ChainCfg cfg;
+    if (chain_pick(&cfg, c->fast_kind, c->ncomp, c->S, c->R, 4, 1))
+      return set_err(c, MR_CONTRACT, "unsupported component count");
+    MR_CUDA_TRY(c, launch_fast_rhs(cfg, in, out, c->ncell, c->ncomp, c->chem, c->fastA, c->stream));
+  }
+  c->launches++;
+  return MR_OK;
+}
+
+// reference_solution (erk.cpp:59-75): erk_integrate (:40-57) of cash-karp5
+// (butcher.cpp:305-321) on sum_rhs (partitioned_system.hpp:41-48) over the
+// device-resident state; erk_step's finite checks (:24-36); no counters.
+int mr_reference_solution(mr_ctx* c, double t0, double tf, double h, int* fail_stage)
+{
+  if (fail_stage) *fail_stage = -1;
+  if (!c) return MR_CONTRACT;
+  if (!c->has_grid) return set_err(c, MR_CONTRACT, "grid not set (mr_grid_set)");
+  if (c->fast_kind < 0 || c->slow_kind < 0)
+    return set_err(c, MR_CONTRACT, "PartitionedSystem: fast/slow plugins not configured");
+  if (c->fast_kind == FK_NONE && c->slow_kind == SK_NONE)
+    return set_err(c, MR_CONTRACT, "PartitionedSystem: at least one partition required");
+  if (!(tf > t0)) return set_err(c, MR_CONTRACT, "erk_integrate: tf must exceed t0");
+  if (!(h > 0.0)) return set_err(c, MR_CONTRACT, "erk_integrate: h must be positive");
+  if (c->slow_kind == SK_STENCIL && c->n0l < c->M)
+    return set_err(c, MR_CONTRACT, "slab thinner than the stencil ghost width");
+  cudaSetDevice(c->device);
+  int rc = ensure_state(c);
+  if (rc) return rc;
+  // cash-karp5, exactly as butcher.cpp:305-321 writes it
+  const int s = 6;
+  double A[6][6] = {{0}}, b[6] = {0}, cc[6] = {0};
+  A[1][0] = 1.0 / 5.0;
+  A[2][0] = 3.0 / 40.0; A[2][1] = 9.0 / 40.0;
+  A[3][0] = 3.0 / 10.0; A[3][1] = -9.0 / 10.0; A[3][2] = 6.0 / 5.0;
+  A[4][0] = -11.0 / 54.0; A[4][1] = 5.0 / 2.0; A[4][2] = -70.0 / 27.0; A[4][3] = 35.0 / 27.0;
+  A[5][0] = 1631.0 / 55296.0; A[5][1] = 175.0 / 512.0; A[5][2] = 575.0 / 13824.0;
+  A[5][3] = 44275.0 / 110592.0; A[5][4] = 253.0 / 4096.0;
+  b[0] = 37.0 / 378.0; b[2] = 250.0 / 621.0; b[3] = 125.0 / 594.0; b[5] = 512.0 / 1771.0;
+  cc[1] = 1.0 / 5.0; cc[2] = 3.0 / 10.0; cc[3] = 3.0 / 5.0; cc[4] = 1.0; cc[5] = 7.0 / 8.0;
+  (void)cc;
+  // buffers: k[0..5], stage, f_fast, f_implicit
+  while ((int)c->rs_bufs.size() < s + 3) {
+    double* p = nullptr;
+    MR_CUDA_TRY(c, cudaMalloc(&p, c->dof * sizeof(double)));
+    c->rs_bufs.push_back(p);
+  }
+  double** k = c->rs_bufs.data();
+  double* stage = c->rs_bufs[s];
+  double* tf_ = c->rs_bufs[s + 1];
+  double* ti_ = c->rs_bufs[s + 2];
+  const bool fast = c->fast_kind != FK_NONE, slow = c->slow_kind != SK_NONE;
+  const bool imp = c->slow_kind == SK_STENCIL && c->imex;
+  cudaStream_t st = c->stream;
+  const long n_steps = (long)std::ceil((tf - t0) / h - 1e-12);
+  double t = t0;
+  for (long n = 0; n < n_steps; ++n) {
+    const double step = (n == n_steps - 1) ? (tf - t) : h;
+    MR_CUDA_TRY(c, cudaMemsetAsync(c->d_fail, 0xFF, sizeof(unsigned long long), st));
+    for (int i = 0; i < s; ++i) {
+      const double* f[MR_MAXREF];
+      double cf[MR_MAXREF];
+      int nref = 0;
+      for (int j = 0; j < i; ++j)
+        if (A[i][j] != 0.0) {
+          f[nref] = k[j];
+          cf[nref++] = step * A[i][j];
+        }
+      MR_CUDA_TRY(c, launch_update(c->y_state, stage, nref, f, cf, c->dof, i, c->d_fail, st));
+      c->launches++;
+      if (fast) {
+        rc = eval_fast_dev(c, stage, tf_);
+        if (rc) return rc;
+      }
+      if (imp) {
+        mr_ctx* cs[1] = {c};
+        const double* yc[1] = {stage};
+        double* oc[1] = {ti_};
+        rc = eval_implicit(cs, 1, yc, oc, st);
+        if (rc) return rc;
+      }
+      if (slow) {
+        mr_ctx* cs[1] = {c};
+        const double* yc[1] = {stage};
+        double* oc[1] = {k[i]};
+        rc = eval_slow(cs, 1, yc, oc, st);
+        if (rc) return rc;
+      }
+      MR_CUDA_TRY(c, launch_sum_rhs(c->dof, fast ? tf_ : nullptr, imp ? ti_ : nullptr,
+                                    slow ? k[i] : nullptr, k[i], st));
+      c->launches++;
+    }
+    {
+      const double* f[MR_MAXREF];
+      double cf[MR_MAXREF];
+      int nref = 0;
+      for (int i = 0; i < s; ++i)
+        if (b[i] != 0.0) {
+          f[nref] = k[i];
+          cf[nref++] = step * b[i];
+        }
+      MR_CUDA_TRY(c, launch_update(c->y_state, c->y_work, nref, f, cf, c->dof, s, c->d_fail, st));
+      c->launches++;
+    }
+    if (c->nranks > 1)
+      MR_NCCL_TRY(c, AllReduce(c->d_fail, c->d_fail, 1, ncclUint64, ncclMin, c->comm, st));
+    MR_CUDA_TRY(c, cudaMemcpyAsync(c->h_fail, c->d_fail, sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, st));
+    MR_CUDA_TRY(c, cudaStreamSynchronize(st));
+    if (*c->h_fail != MR_NO_FAIL) {
+      const int fs = (int)(*c->h_fail >> 40);
+      if (fail_stage) *fail_stage = fs;
+      return set_err(c, MR_INTEGRATION,
+                     fs == s ? "erk_step: non-finite result" : "erk_step: non-finite stage value");
+    }
+    std::swap(c->y_state, c->y_work);
+    t = (n == n_steps - 1) ? tf : t0 + (double)(n + 1) * h;
+  }
   return MR_OK;
 }
 

@@ -88,6 +88,16 @@ def main():
     out["imex_transport_n12_counters"] = cnt
     meta["imex_transport_n12"] = dict(H=H, steps=3, m=4, config="C5", fast="none", **over)
 
+    # 2c. reference_solution (erk.cpp:59-75): cash-karp5 on the summed RHS
+    for key, name, fast, h, nst, over in [
+            ("refsol_C1_n8", "C1", "chem", 2e-17, 10, {}),
+            ("refsol_C3_n8", "C3", "none", 2e-4, 5, {}),
+            ("refsol_C5_n8", "C5", "none", 2e-4, 5, dict(d_impl=0.05, cg_iters=8))]:
+        cfg, sysm = physics_system(name, 8, fast=fast, override=over)
+        y0 = sysm.initial_condition(cfg["ic_seed"])
+        out[key + "_y"] = sysm.reference_solution(0.0, nst * h, h, y0, use_reference=True)
+        meta[key] = dict(config=name, fast=fast, h_ref=h, steps=nst, **over)
+
     # 3. LinearTwoRateOde per cell through the reference mri_integrate
     for cp_name, table, m in [("mis-kw3", "bogacki-shampine3", 10),
                               ("imex-mri-gark4-explicit", "classic-rk4", 10)]:

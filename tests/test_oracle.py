@@ -123,3 +123,18 @@ def test_restatement_equals_reference_live():
     a, ca = sysm.mri_integrate(cp, "classic-rk4", 7, 0.0, 2 * H, H, y0)
     b, cb = sysm.mri_integrate(cp, "classic-rk4", 7, 0.0, 2 * H, H, y0, use_reference=True)
     assert np.array_equal(a, b) and np.array_equal(ca, cb)
+
+
+@pytest.mark.parametrize("key", ["refsol_C1_n8", "refsol_C3_n8", "refsol_C5_n8"])
+def test_reference_solution_fixture_bitwise(key):
+    """reference_solution (erk.cpp:59-75, cash-karp5 on sum_rhs) restated."""
+    from tests.helpers import oracle_system
+    meta = META[key]
+    cfg = dict(CONFIGS[meta["config"]])
+    if "d_impl" in meta:
+        cfg.update(d_impl=meta["d_impl"], cg_iters=meta["cg_iters"])
+    sysm = oracle_system(cfg, 8, fast=meta["fast"])
+    y0 = sysm.initial_condition(cfg["ic_seed"])
+    h = meta["h_ref"]
+    y = sysm.reference_solution(0.0, meta["steps"] * h, h, y0)
+    assert np.array_equal(y, FIX[key + "_y"])
