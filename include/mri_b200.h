@@ -142,6 +142,14 @@ int mr_mri_integrate(mr_ctx* ctx, double t0, double tf, double H, uint64_t* coun
 /* End-to-end variant with HOST buffers: H2D of y_in, the step, D2H of y_out. */
 int mr_mri_step_host(mr_ctx* ctx, double t, double H, const double* y_in, double* y_out,
                      uint64_t* counters, int* fail_stage);
+/* ark_imex_step / ark_imex_integrate (proj/src/mri.cpp:437-557): the
+ * single-rate ARK4(3)6L[2]SA IMEX pair (butcher.cpp:362-427) on the same
+ * plugins -- explicit part f_fast + f_explicit, implicit f_implicit solved
+ * by the device Newton-PCG (mr_slow_implicit_diffusion, mr_newton_config).
+ * Counters accumulate like EvalCounters; state unchanged on failure. */
+int mr_ark_imex_step(mr_ctx* ctx, double t, double H, uint64_t* counters, int* fail_stage);
+int mr_ark_imex_integrate(mr_ctx* ctx, double t0, double tf, double H, uint64_t* counters,
+                          int* fail_stage);
 /* reference_solution (proj/src/erk.cpp:59-75): single-rate cash-karp5
  * (erk_integrate, :40-57) of the summed right-hand side f_fast + f_implicit +
  * f_explicit (partitioned_system.hpp:41-48) from t0 to tf with step h_ref, on

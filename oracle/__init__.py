@@ -102,6 +102,8 @@ def lib():
         for fn in ("orc_sys_mri_step",):
             getattr(L, fn).argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int, C.c_double,
                                        C.c_double, _dp, _u64p, _ip, C.c_char_p, C.c_size_t]
+        L.orc_sys_ark_imex_integrate.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double,
+                                                 _dp, _u64p, _ip, C.c_char_p, C.c_size_t]
         L.orc_sys_reference_solution.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double,
                                                  _dp, _ip, C.c_char_p, C.c_size_t]
         L.orc_sys_mri_integrate.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int,
@@ -138,6 +140,8 @@ def ref():
         L.ref_coupling_info.argtypes = [C.c_char_p, C.c_int, _ip, _ip, _ip, _ip, _dp]
         L.ref_sys_mri_step.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int, C.c_double,
                                        C.c_double, _dp, _u64p, _ip, C.c_char_p, C.c_size_t]
+        L.ref_sys_ark_imex_integrate.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double,
+                                                 _dp, _u64p, _ip, C.c_char_p, C.c_size_t]
         L.ref_sys_reference_solution.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double,
                                                  _dp, _ip, C.c_char_p, C.c_size_t]
         L.ref_sys_mri_integrate.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int,
@@ -300,6 +304,14 @@ class System:
             raise StepError(rc, stage, err, cnt)
         return y2, cnt
 
+
+    def ark_imex_integrate(self, t0, tf, H, y, counters=None, use_reference=False):
+        """ark_imex_integrate (mri.cpp:542-557) with the ark436 pair."""
+        fn = ref().ref_sys_ark_imex_integrate if use_reference else lib().orc_sys_ark_imex_integrate
+        rc, y2, cnt, stage, err = self._call(fn, t0, tf, H, y=y, counters=counters)
+        if rc:
+            raise StepError(rc, stage, err, cnt)
+        return y2, cnt
 
     def reference_solution(self, t0, tf, h_ref, y, use_reference=False):
         """reference_solution (erk.cpp:59-75): cash-karp5 on the summed RHS."""

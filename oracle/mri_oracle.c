@@ -1163,6 +1163,159 @@ int orc_mri_integrate(const orc_coupling* cp, const orc_table* fast, int m, cons
   return rc;
 }
 
+/* ARK4(3)6L[2]SA pair, proj/src/butcher.cpp:362-427 (make_ark436) */
+typedef struct { double AE[6][6], AI[6][6], b[6], c[6]; } ark436;
+static void ark436_tables(ark436* t)
+{
+  memset(t, 0, sizeof(*t));
+  t->c[0] = 0; t->c[1] = 0.5; t->c[2] = 83.0 / 250.0; t->c[3] = 31.0 / 50.0;
+  t->c[4] = 17.0 / 20.0; t->c[5] = 1.0;
+  t->AE[1][0] = 0.5;
+  t->AE[2][0] = 13861.0 / 62500.0;
+  t->AE[2][1] = 6889.0 / 62500.0;
+  t->AE[3][0] = -116923316275.0 / 2393684061468.0;
+  t->AE[3][1] = -2731218467317.0 / 15368042101831.0;
+  t->AE[3][2] = 9408046702089.0 / 11113171139209.0;
+  t->AE[4][0] = -451086348788.0 / 2902428689909.0;
+  t->AE[4][1] = -2682348792572.0 / 7519795681897.0;
+  t->AE[4][2] = 12662868775082.0 / 11960479115383.0;
+  t->AE[4][3] = 3355817975965.0 / 11060851509271.0;
+  t->AE[5][0] = 647845179188.0 / 3216320057751.0;
+  t->AE[5][1] = 73281519250.0 / 8382639484533.0;
+  t->AE[5][2] = 552539513391.0 / 3454668386233.0;
+  t->AE[5][3] = 3354512671639.0 / 8306763924573.0;
+  t->AE[5][4] = 4040.0 / 17871.0;
+  t->b[0] = 82889.0 / 524892.0; t->b[1] = 0.0; t->b[2] = 15625.0 / 83664.0;
+  t->b[3] = 69875.0 / 102672.0; t->b[4] = -2260.0 / 8211.0; t->b[5] = 0.25;
+  t->AI[1][0] = 0.25; t->AI[1][1] = 0.25;
+  t->AI[2][0] = 8611.0 / 62500.0; t->AI[2][1] = -1743.0 / 31250.0; t->AI[2][2] = 0.25;
+  t->AI[3][0] = 5012029.0 / 34652500.0; t->AI[3][1] = -654441.0 / 2922500.0;
+  t->AI[3][2] = 174375.0 / 388108.0; t->AI[3][3] = 0.25;
+  t->AI[4][0] = 15267082809.0 / 155376265600.0; t->AI[4][1] = -71443401.0 / 120774400.0;
+  t->AI[4][2] = 730878875.0 / 902184768.0; t->AI[4][3] = 2285395.0 / 8070912.0;
+  t->AI[4][4] = 0.25;
+  t->AI[5][0] = 82889.0 / 524892.0; t->AI[5][1] = 0.0; t->AI[5][2] = 15625.0 / 83664.0;
+  t->AI[5][3] = 69875.0 / 102672.0; t->AI[5][4] = -2260.0 / 8211.0; t->AI[5][5] = 0.25;
+}
+
+/* combined_explicit of ark_imex_step, proj/src/mri.cpp:450-456:
+ * out = f_fast (or 0); out += 1.0 f_explicit */
+static void combined_explicit(const orc_problem* p, double t, const double* y, double* out,
+                              double* tmp)
+{
+  const size_t dof = p->ncell * (size_t)p->ncomp;
+  if (p->fast_kind != ORC_FAST_NONE) orc_fast_rhs(p, t, y, out);
+  else memset(out, 0, sizeof(double) * dof);
+  if (p->slow_kind != ORC_SLOW_NONE) {
+    orc_slow_rhs(p, t, y, tmp);
+    axpy_into(out, 1.0, tmp, dof);
+  }
+}
+
+/* ark_imex_step, proj/src/mri.cpp:437-522, with newton_pcg_stage as the
+ * ImplicitStageSolver (same Newton iteration; fixed-iteration PCG instead of
+ * GMRES).  y is overwritten on success, untouched on error. */
+int orc_ark_imex_step(const orc_problem* p, double t, double* y, double H, orc_counters* cnt,
+                      int* fail_stage, char* err, size_t errlen)
+{
+  *fail_stage = -1;
+  if (H <= 0.0) { if (err) snprintf(err, errlen, "ark_imex_step: H must be positive"); return ORC_CONTRACT; }
+  if (!(p->slow_kind == ORC_SLOW_STENCIL && p->grid && p->grid->imex)) {
+    if (err) snprintf(err, errlen, "ark_imex_step: f_implicit required");
+    return ORC_CONTRACT;
+  }
+  ark436 tb;
+  ark436_tables(&tb);
+  const int s = 6;
+  const size_t dof = p->ncell * (size_t)p->ncomp;
+  double* fE[6];
+  double* fI[6];
+  for (int i = 0; i < s; ++i) {
+    fE[i] = (double*)malloc(sizeof(double) * dof);
+    fI[i] = (double*)malloc(sizeof(double) * dof);
+  }
+  double* Y = (double*)malloc(sizeof(double) * dof);
+  double* cgw = (double*)malloc(sizeof(double) * dof * 5);
+  int rc = ORC_OK;
+  combined_explicit(p, t, y, fE[0], cgw);
+  ++cnt->n_explicit_evals;
+  orc_implicit_rhs(p, t, y, fI[0]);
+  ++cnt->n_implicit_evals;
+  for (int i = 1; i < s && rc == ORC_OK; ++i) {
+    double* known = cgw;
+    memcpy(known, y, sizeof(double) * dof);
+    for (int j = 0; j < i; ++j) {
+      if (tb.AE[i][j] != 0.0) axpy_into(known, H * tb.AE[i][j], fE[j], dof);
+      if (tb.AI[i][j] != 0.0) axpy_into(known, H * tb.AI[i][j], fI[j], dof);
+    }
+    const double t_stage = t + tb.c[i] * H;
+    if (!orc_all_finite(known, dof)) {
+      if (err) snprintf(err, errlen, "ark_imex_step: non-finite stage data at stage %d", i);
+      *fail_stage = i;
+      rc = ORC_INTEGRATION;
+      break;
+    }
+    const double gamma = H * tb.AI[i][i];
+    const int ok = newton_pcg_stage(p, gamma, known, Y, cgw + dof, cgw + 2 * dof, cgw + 3 * dof,
+                                    cgw + 4 * dof, cnt);
+    ++cnt->n_implicit_solves;
+    if (!ok) {
+      if (err) snprintf(err, errlen, "ark_imex_step: nonlinear solve failed at stage %d", i);
+      *fail_stage = i;
+      rc = ORC_INTEGRATION;
+      break;
+    }
+    memcpy(fI[i], Y, sizeof(double) * dof);
+    axpy_into(fI[i], -1.0, known, dof);
+    for (size_t q = 0; q < dof; ++q) fI[i][q] /= gamma;
+    combined_explicit(p, t_stage, Y, fE[i], cgw + dof);
+    ++cnt->n_explicit_evals;
+  }
+  if (rc == ORC_OK) {
+    memcpy(Y, y, sizeof(double) * dof);
+    for (int j = 0; j < s; ++j) {
+      const double b = tb.b[j];
+      if (b != 0.0) {
+        axpy_into(Y, H * b, fE[j], dof);
+        axpy_into(Y, H * b, fI[j], dof);
+      }
+    }
+    if (!orc_all_finite(Y, dof)) {
+      if (err) snprintf(err, errlen, "ark_imex_step: non-finite result");
+      *fail_stage = s;
+      rc = ORC_INTEGRATION;
+    } else {
+      memcpy(y, Y, sizeof(double) * dof);
+    }
+  }
+  for (int i = 0; i < s; ++i) { free(fE[i]); free(fI[i]); }
+  free(Y); free(cgw);
+  return rc;
+}
+
+/* ark_imex_integrate, proj/src/mri.cpp:542-557 */
+int orc_ark_imex_integrate(const orc_problem* p, double t0, double tf, double H, double* y,
+                           orc_counters* cnt, int* fail_stage, char* err, size_t errlen)
+{
+  *fail_stage = -1;
+  if (tf <= t0) { if (err) snprintf(err, errlen, "ark_imex_integrate: tf must exceed t0"); return ORC_CONTRACT; }
+  const long n_steps = (long)ceil((tf - t0) / H - 1e-12);
+  const size_t dof = p->ncell * (size_t)p->ncomp;
+  double* work = (double*)malloc(sizeof(double) * dof);
+  memcpy(work, y, sizeof(double) * dof);
+  double t = t0;
+  int rc = ORC_OK;
+  for (long i = 0; i < n_steps; ++i) {
+    const double step = (i == n_steps - 1) ? (tf - t) : H;
+    rc = orc_ark_imex_step(p, t, work, step, cnt, fail_stage, err, errlen);
+    if (rc != ORC_OK) break;
+    t = (i == n_steps - 1) ? tf : t0 + (double)(i + 1) * H;
+  }
+  if (rc == ORC_OK) memcpy(y, work, sizeof(double) * dof);
+  free(work);
+  return rc;
+}
+
 /* PartitionedSystem::sum_rhs, proj/include/multirate/partitioned_system.hpp:41-48:
  * out = 0; out += 1.0 f_fast; out += 1.0 f_implicit; out += 1.0 f_explicit */
 static void sum_rhs(const orc_problem* p, double t, const double* y, double* out, double* tmp)
@@ -1380,4 +1533,14 @@ int orc_sys_reference_solution(orc_sys* s, double t0, double tf, double h, doubl
                                int* fail_stage, char* err, size_t errlen)
 {
   return orc_reference_solution(&s->prob, t0, tf, h, y, fail_stage, err, errlen);
+}
+
+int orc_sys_ark_imex_integrate(orc_sys* s, double t0, double tf, double H, double* y,
+                               uint64_t* counters, int* fail_stage, char* err, size_t errlen)
+{
+  orc_counters c;
+  counters_in(counters, &c);
+  const int rc = orc_ark_imex_integrate(&s->prob, t0, tf, H, y, &c, fail_stage, err, errlen);
+  counters_out(&c, counters);
+  return rc;
 }

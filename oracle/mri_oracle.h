@@ -220,6 +220,13 @@ int orc_sys_initial_condition(orc_sys* s, uint64_t seed, double* Y);
 int orc_sys_mri_step(orc_sys* s, const char* coupling, const char* fast_table, int m,
                      double t, double H, double* y, uint64_t* counters, int* fail_stage,
                      char* err, size_t errlen);
+/* ark_imex_step / ark_imex_integrate (proj/src/mri.cpp:437-557), ARK4(3)6L[2]SA */
+int orc_ark_imex_step(const orc_problem* p, double t, double* y, double H, orc_counters* cnt,
+                      int* fail_stage, char* err, size_t errlen);
+int orc_ark_imex_integrate(const orc_problem* p, double t0, double tf, double H, double* y,
+                           orc_counters* cnt, int* fail_stage, char* err, size_t errlen);
+int orc_sys_ark_imex_integrate(orc_sys* s, double t0, double tf, double H, double* y,
+                               uint64_t* counters, int* fail_stage, char* err, size_t errlen);
 /* reference_solution (proj/src/erk.cpp:59-75): cash-karp5 on sum_rhs */
 int orc_reference_solution(const orc_problem* p, double t0, double tf, double h, double* y,
                            int* fail_stage, char* err, size_t errlen);

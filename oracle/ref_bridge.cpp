@@ -282,3 +282,22 @@ extern "C" int ref_sys_reference_solution(orc_sys* sys, double t0, double tf, do
     std::memcpy(y, out.data(), sizeof(double) * ps.dimension);
   });
 }
+
+// multirate::ark_imex_integrate (mri.cpp:542-557) with the registered ark436 pair
+extern "C" int ref_sys_ark_imex_integrate(orc_sys* sys, double t0, double tf, double H, double* y,
+                                          uint64_t* counters, int* fail_stage, char* err,
+                                          size_t errlen)
+{
+  EvalCounters c = counters_from(counters);
+  const int rc = guarded(err, errlen, fail_stage, [&] {
+    PartitionedSystem ps = make_system(sys);
+    StateVector yv(ps.dimension);
+    std::memcpy(yv.data(), y, sizeof(double) * ps.dimension);
+    ImplicitStageSolver solver = stage_solver(sys, yv);
+    const ArkPair pair = lookup_ark_pair("ark436-imex-pair");
+    StateVector out = ark_imex_integrate(pair, ps, solver, t0, tf, H, yv, c);
+    std::memcpy(y, out.data(), sizeof(double) * ps.dimension);
+  });
+  counters_to(c, counters);
+  return rc;
+}

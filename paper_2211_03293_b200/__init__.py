@@ -95,6 +95,8 @@ def lib():
         "mr_implicit_rhs": (C.c_int, [vp, C.c_double, _dp, _dp]),
         "mr_newton_config": (C.c_int, [vp, C.c_double, C.c_double, C.c_int, _dp]),
         "mr_reference_solution": (C.c_int, [vp, C.c_double, C.c_double, C.c_double, _ip]),
+        "mr_ark_imex_step": (C.c_int, [vp, C.c_double, C.c_double, _u64p, _ip]),
+        "mr_ark_imex_integrate": (C.c_int, [vp, C.c_double, C.c_double, C.c_double, _u64p, _ip]),
         "mr_state_upload": (C.c_int, [vp, _dp]),
         "mr_state_download": (C.c_int, [vp, _dp]),
         "mr_state_device_ptr": (C.c_void_p, [vp]),
@@ -370,6 +372,21 @@ class Context:
         stage = C.c_int(-1)
         rc = self.L.mr_mri_step_host(self.h, t, H, _p(y_in), _p(y_out), _p(cnt, _u64p),
                                      C.byref(stage))
+        self._check(rc, stage.value)
+        return cnt
+
+    def ark_imex_step(self, t, H, counters=None):
+        """ark_imex_step (mri.cpp:437-522), ARK4(3)6L[2]SA, device state."""
+        cnt = self.counters() if counters is None else counters
+        stage = C.c_int(-1)
+        rc = self.L.mr_ark_imex_step(self.h, t, H, _p(cnt, _u64p), C.byref(stage))
+        self._check(rc, stage.value)
+        return cnt
+
+    def ark_imex_integrate(self, t0, tf, H, counters=None):
+        cnt = self.counters() if counters is None else counters
+        stage = C.c_int(-1)
+        rc = self.L.mr_ark_imex_integrate(self.h, t0, tf, H, _p(cnt, _u64p), C.byref(stage))
         self._check(rc, stage.value)
         return cnt
 

@@ -198,6 +198,7 @@ cudaError_t launch_gathered_sum(const double* g, int n, double* sc, int slot, cu
 cudaError_t launch_scalar_copy(double* sc, int dst, int src, cudaStream_t st);
 cudaError_t launch_sum_rhs(size_t n, const double* ff, const double* fi, const double* fe,
                            double* out, cudaStream_t st);
+cudaError_t launch_add2(size_t n, const double* a, const double* b, double* out, cudaStream_t st);
 cudaError_t launch_recover_fi(size_t n, double gamma, const double* Y, const double* known,
                               double* fI, int mri_stage, unsigned long long* fail,
                               cudaStream_t st);

@@ -645,6 +645,19 @@ static __global__ void __launch_bounds__(256) sum_rhs_kernel(size_t n, const dou
   }
 }
 
+// combined_explicit of ark_imex_step (mri.cpp:450-456): out = f_fast (or 0);
+// out += 1.0 f_explicit (absent operands: null)
+static __global__ void __launch_bounds__(256) add2_kernel(size_t n, const double* a,
+                                                          const double* b, double* out)
+{
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    double o = a ? a[i] : 0.0;
+    if (b) o = __dadd_rn(o, __dmul_rn(1.0, b[i]));
+    out[i] = o;
+  }
+}
+
 int lap_blocks() { return kLapBlocks; }
 
 cudaError_t launch_lap7(int mode, const LapArgs& a, const double* y, const double* lo,
@@ -707,6 +720,15 @@ cudaError_t launch_sum_rhs(size_t n, const double* ff, const double* fi, const d
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks == 0) blocks = 1;
   sum_rhs_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, ff, fi, fe, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add2(size_t n, const double* a, const double* b, double* out, cudaStream_t st)
+{
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks == 0) blocks = 1;
+  add2_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, a, b, out);
   return cudaGetLastError();
 }
 

@@ -190,6 +190,7 @@ struct mr_ctx {
   double* cg_gather = nullptr;  // [nranks] for the cross-rank fixed-order sum
   double* newton_w = nullptr;   // ImplicitStageSolver::weights (local slab); null = unit
   std::vector<double*> rs_bufs;  // reference solution: k[6], stage, f_fast, f_implicit
+  std::vector<double*> ark_bufs; // ARK-IMEX: fE[6], fI[6], f_fast
   double newton_tol = 1.0e-10;  // NewtonConfig defaults (solvers.hpp:19-23)
   double newton_safety = 0.1;
   int newton_max = 10;
@@ -276,6 +277,8 @@ void free_state(mr_ctx* c)
   free_dev_t(c->newton_w);  // weights are per grid
   for (auto& p : c->rs_bufs) free_dev_t(p);
   c->rs_bufs.clear();
+  for (auto& p : c->ark_bufs) free_dev_t(p);
+  c->ark_bufs.clear();
   c->halo_elems = 0;
   c->state_valid = false;
 }
@@ -761,36 +764,24 @@ int dot_finalize(mr_ctx** cs, int n, int slot, cudaStream_t st, bool second = fa
   return MR_OK;
 }
 
-// ImplicitSolve stage i (mri.cpp:378-421): known, then newton_solve
-// (solvers.cpp:150-208) from Y = known with the fixed-iteration PCG as the
-// linear solver (same iteration as oracle newton_pcg_stage), then
-// fI_i = (Y - known)/gamma.  The convergence test is a host decision on the
-// globally reduced WRMS (one 8-byte read per Newton iteration; every slab and
-// rank sees the same value).  *host_key is set when Newton fails.
-int solve_stage(mr_ctx** cs, int n, int i, double t, double H, const Plan& plan,
-                std::vector<const double*>& ycur, cudaStream_t st, unsigned long long* host_key)
+// newton_solve (solvers.cpp:150-208) on G(Y) = Y - gamma f_I(Y) - known with
+// known in cg_known and Y (initialised by the caller, = known) in y_work; the
+// linear solve is the fixed-iteration PCG (same iteration as oracle
+// newton_pcg_stage).  Convergence is a host decision on the globally reduced
+// WRMS (one 8-byte read per Newton iteration; every slab and rank sees the
+// same value).  On success fI = (Y - known)/gamma (mri.cpp:418-421) goes to
+// fI_out[r]; on failure *host_key = (stage, 0, 2).  Counts go to
+// solve_evals[i] / solve_nl[i].
+int newton_pcg(mr_ctx** cs, int n, int i, double gamma, double* const* fI_out,
+               unsigned long long* host_key, cudaStream_t st)
 {
   mr_ctx* c0 = cs[0];
-  const double gamma = H * c0->cp.gbar[i][i];
   const double target = c0->newton_safety * c0->newton_tol;
   const double nglob = (double)c0->n0 * c0->n1 * c0->n2 * c0->ncomp;
   std::vector<const double*> lo(n), hi(n), src(n);
   for (int r = 0; r < n; ++r) {
-    mr_ctx* c = cs[r];
-    int rc = ensure_cg(c);
-    if (rc) return rc;
-    ChainStageDev sd;
-    fill_chain_stage(c, i, t, H, plan, sd);
-    const double* f[MR_MAXREF];
-    for (int q = 0; q < sd.nref; ++q) f[q] = c->slots[sd.ref_slot[q]];
-    MR_CUDA_TRY(c, launch_update(ycur[r], c->cg_known, sd.nref, f, sd.coef[0], c->dof, i,
-                                 c->d_fail, st));
-    MR_CUDA_TRY(c, cudaMemcpyAsync(c->y_work, c->cg_known, c->dof * sizeof(double),
-                                   cudaMemcpyDeviceToDevice, st));
-    c->launches++;
-    ycur[r] = c->y_work;
-    c->solve_evals[i] = 0;
-    c->solve_nl[i] = 0;
+    cs[r]->solve_evals[i] = 0;
+    cs[r]->solve_nl[i] = 0;
   }
   bool converged = false;
   for (int iter = 0; iter <= c0->newton_max; ++iter) {
@@ -855,11 +846,38 @@ int solve_stage(mr_ctx** cs, int n, int i, double t, double H, const Plan& plan,
   }
   for (int r = 0; r < n; ++r) {
     mr_ctx* c = cs[r];
-    double* fI = plan.islot_of[i] >= 0 ? c->slots[plan.islot_of[i]] : c->cg_q;
-    MR_CUDA_TRY(c, launch_recover_fi(c->dof, gamma, c->y_work, c->cg_known, fI, i, c->d_fail, st));
+    MR_CUDA_TRY(c, launch_recover_fi(c->dof, gamma, c->y_work, c->cg_known, fI_out[r], i, c->d_fail,
+                                     st));
     c->launches++;
   }
   return MR_OK;
+}
+
+// ImplicitSolve stage i (mri.cpp:378-421): known, then newton_pcg from
+// Y = known.  *host_key is set when Newton fails.
+int solve_stage(mr_ctx** cs, int n, int i, double t, double H, const Plan& plan,
+                std::vector<const double*>& ycur, cudaStream_t st, unsigned long long* host_key)
+{
+  const double gamma = H * cs[0]->cp.gbar[i][i];
+  for (int r = 0; r < n; ++r) {
+    mr_ctx* c = cs[r];
+    int rc = ensure_cg(c);
+    if (rc) return rc;
+    ChainStageDev sd;
+    fill_chain_stage(c, i, t, H, plan, sd);
+    const double* f[MR_MAXREF];
+    for (int q = 0; q < sd.nref; ++q) f[q] = c->slots[sd.ref_slot[q]];
+    MR_CUDA_TRY(c, launch_update(ycur[r], c->cg_known, sd.nref, f, sd.coef[0], c->dof, i,
+                                 c->d_fail, st));
+    MR_CUDA_TRY(c, cudaMemcpyAsync(c->y_work, c->cg_known, c->dof * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, st));
+    c->launches++;
+    ycur[r] = c->y_work;
+  }
+  std::vector<double*> fI_out(n);
+  for (int r = 0; r < n; ++r)
+    fI_out[r] = plan.islot_of[i] >= 0 ? cs[r]->slots[plan.islot_of[i]] : cs[r]->cg_q;
+  return newton_pcg(cs, n, i, gamma, fI_out.data(), host_key, st);
 }
 
 // One slow step over a domain of slab contexts sharing a device stream (n > 1)
@@ -1613,6 +1631,236 @@ int mr_mri_integrate(mr_ctx* c, double t0, double tf, double H, uint64_t* counte
   for (long i = 0; i < n_steps; ++i) {
     const double step = (i == n_steps - 1) ? (tf - t) : H;
     rc = mr_mri_step(c, t, step, counters, fail_stage);
+    if (rc) break;
+    t = (i == n_steps - 1) ? tf : t0 + static_cast<double>(i + 1) * H;
+  }
+  if (backup) {
+    if (rc)
+      cudaMemcpyAsync(c->y_state, backup, c->dof * sizeof(double), cudaMemcpyDeviceToDevice,
+                      c->stream);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(backup);
+  }
+  return rc;
+}
+
+static int eval_fast_dev(mr_ctx* c, const double* in, double* out);
+
+// ---------------------------------------------------------------------------
+// ARK-IMEX: ark_imex_step (mri.cpp:437-522) with the
+// ARK4(3)6L[2]SA pair (butcher.cpp:362-427) on the same device plugins --
+// combined explicit part f_fast + f_explicit, implicit f_implicit solved by
+// newton_pcg (the stage solver of the IMEX MRI path).
+// ---------------------------------------------------------------------------
+namespace {
+struct Ark436 {
+  double AE[6][6] = {}, AI[6][6] = {}, b[6] = {}, c[6] = {};
+  Ark436()
+  {
+    c[1] = 0.5; c[2] = 83.0 / 250.0; c[3] = 31.0 / 50.0; c[4] = 17.0 / 20.0; c[5] = 1.0;
+    AE[1][0] = 0.5;
+    AE[2][0] = 13861.0 / 62500.0; AE[2][1] = 6889.0 / 62500.0;
+    AE[3][0] = -116923316275.0 / 2393684061468.0;
+    AE[3][1] = -2731218467317.0 / 15368042101831.0;
+    AE[3][2] = 9408046702089.0 / 11113171139209.0;
+    AE[4][0] = -451086348788.0 / 2902428689909.0;
+    AE[4][1] = -2682348792572.0 / 7519795681897.0;
+    AE[4][2] = 12662868775082.0 / 11960479115383.0;
+    AE[4][3] = 3355817975965.0 / 11060851509271.0;
+    AE[5][0] = 647845179188.0 / 3216320057751.0;
+    AE[5][1] = 73281519250.0 / 8382639484533.0;
+    AE[5][2] = 552539513391.0 / 3454668386233.0;
+    AE[5][3] = 3354512671639.0 / 8306763924573.0;
+    AE[5][4] = 4040.0 / 17871.0;
+    b[0] = 82889.0 / 524892.0; b[2] = 15625.0 / 83664.0; b[3] = 69875.0 / 102672.0;
+    b[4] = -2260.0 / 8211.0; b[5] = 0.25;
+    AI[1][0] = 0.25; AI[1][1] = 0.25;
+    AI[2][0] = 8611.0 / 62500.0; AI[2][1] = -1743.0 / 31250.0; AI[2][2] = 0.25;
+    AI[3][0] = 5012029.0 / 34652500.0; AI[3][1] = -654441.0 / 2922500.0;
+    AI[3][2] = 174375.0 / 388108.0; AI[3][3] = 0.25;
+    AI[4][0] = 15267082809.0 / 155376265600.0; AI[4][1] = -71443401.0 / 120774400.0;
+    AI[4][2] = 730878875.0 / 902184768.0; AI[4][3] = 2285395.0 / 8070912.0; AI[4][4] = 0.25;
+    AI[5][0] = 82889.0 / 524892.0; AI[5][2] = 15625.0 / 83664.0; AI[5][3] = 69875.0 / 102672.0;
+    AI[5][4] = -2260.0 / 8211.0; AI[5][5] = 0.25;
+  }
+};
+
+// combined_explicit (mri.cpp:450-456) of every context's `in` into `out`
+int ark_explicit(mr_ctx** cs, int n, double* const* in, double* const* out, cudaStream_t st)
+{
+  const bool fast = cs[0]->fast_kind != FK_NONE, slow = cs[0]->slow_kind != SK_NONE;
+  for (int r = 0; r < n && fast; ++r) {
+    int rc = eval_fast_dev(cs[r], in[r], cs[r]->ark_bufs[12]);
+    if (rc) return rc;
+  }
+  if (slow) {
+    std::vector<const double*> yc(in, in + n);
+    int rc = eval_slow(cs, n, yc.data(), out, st);
+    if (rc) return rc;
+  }
+  for (int r = 0; r < n; ++r) {
+    MR_CUDA_TRY(cs[r], launch_add2(cs[r]->dof, fast ? cs[r]->ark_bufs[12] : nullptr,
+                                   slow ? out[r] : nullptr, out[r], st));
+    cs[r]->launches++;
+  }
+  return MR_OK;
+}
+
+int ark_domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int* fail_stage)
+{
+  mr_ctx* c0 = cs[0];
+  if (fail_stage) *fail_stage = -1;
+  if (!(H > 0.0)) return set_err(c0, MR_CONTRACT, "ark_imex_step: H must be positive");
+  for (int r = 0; r < n; ++r) {
+    mr_ctx* c = cs[r];
+    if (!c->has_grid) return set_err(c0, MR_CONTRACT, "grid not set (mr_grid_set)");
+    if (c->fast_kind < 0 || c->slow_kind < 0)
+      return set_err(c0, MR_CONTRACT, "PartitionedSystem: fast/slow plugins not configured");
+    if (!(c->slow_kind == SK_STENCIL && c->imex))
+      return set_err(c0, MR_CONTRACT, "ark_imex_step: f_implicit required");
+    int rc = ensure_state(c);
+    if (rc) return rc;
+    rc = ensure_cg(c);
+    if (rc) return rc;
+    while ((int)c->ark_bufs.size() < 13) {
+      double* p = nullptr;
+      MR_CUDA_TRY(c, cudaMalloc(&p, c->dof * sizeof(double)));
+      c->ark_bufs.push_back(p);
+    }
+    MR_CUDA_TRY(c, cudaMemsetAsync(c->d_fail, 0xFF, sizeof(unsigned long long), c0->stream));
+  }
+  static const Ark436 tb;
+  const int s = 6;
+  cudaStream_t st = c0->stream;
+  std::vector<double*> in(n), out(n);
+  uint64_t cnt[8] = {}, snap[7][8] = {};
+  unsigned long long host_key = MR_NO_FAIL;
+  // stage 0: fE_0 = combined(y), fI_0 = f_I(y)
+  for (int r = 0; r < n; ++r) {
+    in[r] = cs[r]->y_state;
+    out[r] = cs[r]->ark_bufs[0];
+  }
+  int rc = ark_explicit(cs, n, in.data(), out.data(), st);
+  if (rc) return rc;
+  cnt[MR_CNT_EXPLICIT_EVALS]++;
+  {
+    std::vector<const double*> yc(n);
+    for (int r = 0; r < n; ++r) {
+      yc[r] = cs[r]->y_state;
+      out[r] = cs[r]->ark_bufs[6];
+    }
+    rc = eval_implicit(cs, n, yc.data(), out.data(), st);
+    if (rc) return rc;
+  }
+  cnt[MR_CNT_IMPLICIT_EVALS]++;
+  for (int i = 1; i < s; ++i) {
+    std::memcpy(snap[i], cnt, sizeof(cnt));
+    // known = y + sum_j H (AE_ij fE_j, then AI_ij fI_j)   (mri.cpp:467-471)
+    for (int r = 0; r < n; ++r) {
+      mr_ctx* c = cs[r];
+      const double* f[MR_MAXREF];
+      double cf[MR_MAXREF];
+      int nref = 0;
+      for (int j = 0; j < i; ++j) {
+        if (tb.AE[i][j] != 0.0) { f[nref] = c->ark_bufs[j]; cf[nref++] = H * tb.AE[i][j]; }
+        if (tb.AI[i][j] != 0.0) { f[nref] = c->ark_bufs[6 + j]; cf[nref++] = H * tb.AI[i][j]; }
+      }
+      MR_CUDA_TRY(c, launch_update(c->y_state, c->cg_known, nref, f, cf, c->dof, i, c->d_fail, st));
+      MR_CUDA_TRY(c, cudaMemcpyAsync(c->y_work, c->cg_known, c->dof * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, st));
+      c->launches++;
+      out[r] = c->ark_bufs[6 + i];
+    }
+    rc = newton_pcg(cs, n, i, H * tb.AI[i][i], out.data(), &host_key, st);
+    if (rc) return rc;
+    const uint64_t nl = (uint64_t)c0->solve_nl[i];
+    cnt[MR_CNT_IMPLICIT_EVALS] += (uint64_t)c0->solve_evals[i];
+    cnt[MR_CNT_NONLINEAR_ITERS] += nl;
+    cnt[MR_CNT_LINEAR_ITERS] += nl * (uint64_t)c0->cg_iters;
+    cnt[MR_CNT_PRECOND_SOLVES] += nl * ((uint64_t)c0->cg_iters + 1);
+    cnt[MR_CNT_IMPLICIT_SOLVES]++;
+    if (host_key != MR_NO_FAIL) break;
+    // fE_i = combined(t + c_i H, Y)
+    for (int r = 0; r < n; ++r) {
+      in[r] = cs[r]->y_work;
+      out[r] = cs[r]->ark_bufs[i];
+    }
+    rc = ark_explicit(cs, n, in.data(), out.data(), st);
+    if (rc) return rc;
+    cnt[MR_CNT_EXPLICIT_EVALS]++;
+  }
+  if (host_key == MR_NO_FAIL) {
+    // out = y + sum_j H b_j (fE_j, then fI_j)   (mri.cpp:510-516)
+    for (int r = 0; r < n; ++r) {
+      mr_ctx* c = cs[r];
+      const double* f[MR_MAXREF];
+      double cf[MR_MAXREF];
+      int nref = 0;
+      for (int j = 0; j < s; ++j)
+        if (tb.b[j] != 0.0) {
+          f[nref] = c->ark_bufs[j]; cf[nref++] = H * tb.b[j];
+          f[nref] = c->ark_bufs[6 + j]; cf[nref++] = H * tb.b[j];
+        }
+      MR_CUDA_TRY(c, launch_update(c->y_state, c->y_work, nref, f, cf, c->dof, s, c->d_fail, st));
+      c->launches++;
+    }
+  }
+  unsigned long long key = MR_NO_FAIL;
+  if (n == 1 && c0->nranks > 1)
+    MR_NCCL_TRY(c0, AllReduce(c0->d_fail, c0->d_fail, 1, ncclUint64, ncclMin, c0->comm, st));
+  for (int r = 0; r < n; ++r)
+    MR_CUDA_TRY(cs[r], cudaMemcpyAsync(cs[r]->h_fail, cs[r]->d_fail, sizeof(unsigned long long),
+                                       cudaMemcpyDeviceToHost, st));
+  MR_CUDA_TRY(c0, cudaStreamSynchronize(st));
+  for (int r = 0; r < n; ++r) key = std::min(key, *cs[r]->h_fail);
+  key = std::min(key, host_key);
+  if (key != MR_NO_FAIL) {
+    const int fs = (int)(key >> 40), inner = (int)(key & 0xFFull);
+    const uint64_t* part = (fs < s && inner == 0) ? snap[fs] : cnt;
+    if (counters)
+      for (int q = 0; q < 8; ++q) counters[q] += part[q];
+    if (fail_stage) *fail_stage = fs;
+    if (fs == s) return set_err(c0, MR_INTEGRATION, "ark_imex_step: non-finite result");
+    if (inner == 0)
+      return set_err(c0, MR_INTEGRATION,
+                     "ark_imex_step: non-finite stage data at stage " + std::to_string(fs));
+    return set_err(c0, MR_INTEGRATION,
+                   "ark_imex_step: nonlinear solve failed at stage " + std::to_string(fs));
+  }
+  if (counters)
+    for (int q = 0; q < 8; ++q) counters[q] += cnt[q];
+  for (int r = 0; r < n; ++r) std::swap(cs[r]->y_state, cs[r]->y_work);
+  return MR_OK;
+}
+}  // namespace
+
+int mr_ark_imex_step(mr_ctx* c, double t, double H, uint64_t* counters, int* fail_stage)
+{
+  if (!c) return MR_CONTRACT;
+  cudaSetDevice(c->device);
+  return ark_domain_step(&c, 1, t, H, counters, fail_stage);
+}
+
+int mr_ark_imex_integrate(mr_ctx* c, double t0, double tf, double H, uint64_t* counters,
+                          int* fail_stage)
+{
+  if (!c) return MR_CONTRACT;
+  if (fail_stage) *fail_stage = -1;
+  if (!(tf > t0)) return set_err(c, MR_CONTRACT, "ark_imex_integrate: tf must exceed t0");
+  cudaSetDevice(c->device);
+  int rc = ensure_state(c);
+  if (rc) return rc;
+  const long n_steps = static_cast<long>(std::ceil((tf - t0) / H - 1e-12));
+  double* backup = nullptr;
+  if (n_steps > 1) {
+    MR_CUDA_TRY(c, cudaMalloc(&backup, c->dof * sizeof(double)));
+    MR_CUDA_TRY(c, cudaMemcpyAsync(backup, c->y_state, c->dof * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, c->stream));
+  }
+  double t = t0;
+  for (long i = 0; i < n_steps; ++i) {
+    const double step = (i == n_steps - 1) ? (tf - t) : H;
+    rc = ark_domain_step(&c, 1, t, step, counters, fail_stage);
     if (rc) break;
     t = (i == n_steps - 1) ? tf : t0 + static_cast<double>(i + 1) * H;
   }

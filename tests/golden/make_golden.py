@@ -98,6 +98,18 @@ def main():
         out[key + "_y"] = sysm.reference_solution(0.0, nst * h, h, y0, use_reference=True)
         meta[key] = dict(config=name, fast=fast, h_ref=h, steps=nst, **over)
 
+    # 2d. ark_imex_integrate (mri.cpp:437-557), ARK4(3)6L[2]SA on the C5 split
+    for key, fast, H, nst, over in [
+            ("ark_transport_n8", "none", 2e-3, 3, dict(d_impl=0.05, cg_iters=8)),
+            ("ark_C5_n8", "chem", 3e-17, 2, {})]:
+        cfg, sysm = physics_system("C5", 8, fast=fast, override=over)
+        y0 = sysm.initial_condition(cfg["ic_seed"])
+        y, cnt = sysm.ark_imex_integrate(0.0, nst * H, H, y0, use_reference=True)
+        out[key + "_y"] = y
+        out[key + "_counters"] = cnt
+        meta[key] = dict(fast=fast, H=H, steps=nst, d_impl=cfg["d_impl"], cg_iters=cfg["cg_iters"])
+        print(key, "counters", cnt.tolist())
+
     # 3. LinearTwoRateOde per cell through the reference mri_integrate
     for cp_name, table, m in [("mis-kw3", "bogacki-shampine3", 10),
                               ("imex-mri-gark4-explicit", "classic-rk4", 10)]:

@@ -160,3 +160,51 @@ def test_virtual_rank_slabs_match_single(P_):
         i0, n0l = P.slab_bounds(n, P_, r)
         got = c.download().reshape(cfg["S"] + 1, n0l, n, n)
         assert per_species_rel_err(got, ref[:, i0:i0 + n0l], cfg["S"] + 1) <= 1e-13
+
+
+# ----------------------------------------------------- ARK-IMEX (8(f) row 4)
+@pytest.mark.parametrize("key", ["ark_transport_n8", "ark_C5_n8"])
+def test_ark_imex_matches_oracle_and_reference(key):
+    meta = META[key]
+    cfg0 = c5(d_impl=meta["d_impl"], cg_iters=meta["cg_iters"])
+    ctx, cfg, y0 = gpu_case(8, cfg0, fast=meta["fast"] == "chem")
+    sysm = oracle_system(cfg, 8, fast=meta["fast"], y0=y0)
+    H = meta["H"]
+    y_ref, cnt_ref = sysm.ark_imex_integrate(0.0, meta["steps"] * H, H, y0)
+    cnt = ctx.ark_imex_integrate(0.0, meta["steps"] * H, H)
+    y = ctx.download()
+    assert np.array_equal(cnt, cnt_ref)
+    assert per_species_rel_err(y, y_ref, cfg["S"] + 1) <= STEP_TOL * meta["steps"]
+    assert solver_counts_ok(cnt, FIX[key + "_counters"], meta["cg_iters"])
+    assert per_species_rel_err(y, FIX[key + "_y"], cfg["S"] + 1) <= STEP_TOL * meta["steps"]
+
+
+def test_ark_imex_failures():
+    cfg0 = c5(d_impl=0.05, cg_iters=0)
+    ctx, cfg, y0 = gpu_case(8, cfg0, fast=False)
+    sysm = oracle_system(cfg, 8, fast="none", y0=y0)
+    with pytest.raises(O.StepError) as eo:
+        sysm.ark_imex_integrate(0.0, 2e-3, 2e-3, y0)
+    cnt = ctx.counters()
+    with pytest.raises(P.IntegrationError) as eg:
+        ctx.ark_imex_step(0.0, 2e-3, cnt)
+    assert eg.value.stage_index == eo.value.stage == 1
+    assert "nonlinear solve failed" in str(eg.value)
+    assert np.array_equal(cnt, eo.value.counters)
+    assert np.array_equal(ctx.download(), y0)
+    # non-finite stage data (before the solve) keeps the earlier counts
+    bad = y0.copy()
+    bad[3] = np.inf
+    ctx.upload(bad)
+    cnt = ctx.counters()
+    with pytest.raises(P.IntegrationError) as eg:
+        ctx.ark_imex_step(0.0, 2e-3, cnt)
+    with pytest.raises(O.StepError) as eo:
+        sysm.ark_imex_integrate(0.0, 2e-3, 2e-3, bad)
+    assert eg.value.stage_index == eo.value.stage
+    assert np.array_equal(cnt, eo.value.counters)
+    # f_implicit required
+    ctx2 = P.Context(0)
+    P.setup_workload(ctx2, "C4", n=8)
+    with pytest.raises(P.ContractError):
+        ctx2.ark_imex_step(0.0, 1e-17)

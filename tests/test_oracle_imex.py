@@ -129,3 +129,17 @@ def test_imex_live_against_reference():
     b, cb = sysm.mri_integrate(GARK3B, "kutta3", 3, 0.0, 2 * H, H, y0, use_reference=True)
     assert per_species_rel_err(a, b, cfg["S"] + 1) <= 1e-12
     assert solver_counts_ok(ca, cb, 12)
+
+
+@pytest.mark.parametrize("key", ["ark_transport_n8", "ark_C5_n8"])
+def test_ark_imex_fixture(key):
+    """ark_imex_integrate (mri.cpp:437-557) restated with the Newton-PCG stage
+    solver against the reference's own run (Newton-GMRES)."""
+    meta = META[key]
+    cfg, sysm, y0 = imex_case(8, fast=meta["fast"], d_impl=meta["d_impl"], cg_iters=meta["cg_iters"])
+    H = meta["H"]
+    y, cnt = sysm.ark_imex_integrate(0.0, meta["steps"] * H, H, y0)
+    assert solver_counts_ok(cnt, FIX[key + "_counters"], meta["cg_iters"])
+    assert per_species_rel_err(y, FIX[key + "_y"], cfg["S"] + 1) <= 1e-13
+    if cnt[4] == 0:  # no Newton iteration taken: identical arithmetic
+        assert np.array_equal(y, FIX[key + "_y"])
