@@ -190,6 +190,41 @@ inline StateVector mri_integrate(Device& d, const MriMethodConfig& mc,
   return mri_integrate(d, mc, t0, tf, H, y0, counters);
 }
 
+// reference_solution (erk.cpp:59-75) on the device plugins: cash-karp5 of
+// f_fast + f_implicit + f_explicit from t0 to tf with step h_ref.
+inline StateVector reference_solution(Device& d, const StateVector& y0, double t0, double tf,
+                                      double h_ref)
+{
+  if (y0.size() != d.dof()) throw ContractError("reference_solution: state size != grid dof");
+  d.check(mr_state_upload(d.ctx(), y0.data()));
+  int stage = -1;
+  const int rc = mr_reference_solution(d.ctx(), t0, tf, h_ref, &stage);
+  d.check(rc, stage);
+  StateVector out(y0.size());
+  d.check(mr_state_download(d.ctx(), out.data()));
+  return out;
+}
+
+// ark_imex_integrate (mri.cpp:542-557) with the ark436 pair
+// (lookup_ark_pair("ark436-imex-pair")) on the device plugins
+inline StateVector ark_imex_integrate(Device& d, const ImplicitStageSolver& solver, double t0,
+                                      double tf, double H, const StateVector& y0,
+                                      EvalCounters& counters)
+{
+  if (y0.size() != d.dof()) throw ContractError("ark_imex_integrate: state size != grid dof");
+  d.solver(solver);
+  d.check(mr_state_upload(d.ctx(), y0.data()));
+  uint64_t c[8];
+  to_c(counters, c);
+  int stage = -1;
+  const int rc = mr_ark_imex_integrate(d.ctx(), t0, tf, H, c, &stage);
+  from_c(c, counters);
+  d.check(rc, stage);
+  StateVector out(y0.size());
+  d.check(mr_state_download(d.ctx(), out.data()));
+  return out;
+}
+
 // "Mode A": the reference's PartitionedSystem (partitioned_system.hpp:25-61)
 // whose f_fast / f_explicit callbacks evaluate the device plugins.
 inline PartitionedSystem partitioned_system(Device& d)

@@ -154,3 +154,105 @@ extern "C" int facade_selftest(int n, int S, int R, double rho, const double* sp
     return 1;
   }
 }
+
+// reference_solution and ark_imex_integrate through the facade (device) vs the
+// reference's own implementations on the CPU physics.  which = 0: reference
+// solution (steps of h); 1: ARK-IMEX (steps of h, IMEX split d_impl).
+extern "C" int facade_selftest2(int which, int n, int S, int R, double rho, const double* species,
+                                const double* reactions, const int* rspecies,
+                                const double* y0in, int order, double diffusion, double d_impl,
+                                int cg_iters, int fast, double h, int steps, const double* newton,
+                                const double* weights, double* errs, uint64_t* counters,
+                                char* err, size_t errlen)
+{
+  try {
+    const int ncomp = S + 1;
+    const size_t dof = (size_t)n * n * n * ncomp;
+    StateVector y0(dof);
+    std::memcpy(y0.data(), y0in, dof * sizeof(double));
+    const double u[3] = {1.0, 1.0, 1.0};
+    const bool imex = d_impl >= 0.0;
+    b200::Device dev(0);
+    dev.grid(n, n, n, ncomp);
+    dev.chemistry(S, R, rho, species, reactions, rspecies);
+    if (!fast) dev.no_fast();
+    dev.stencil(order, diffusion, u);
+    if (imex) dev.implicit_diffusion(d_impl, cg_iters);
+
+    orc_sys_cfg cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.n0 = cfg.n1 = cfg.n2 = n;
+    cfg.n0_global = n;
+    cfg.ncomp = ncomp;
+    cfg.length = 1.0;
+    cfg.fast_kind = fast ? ORC_FAST_CHEM : ORC_FAST_NONE;
+    cfg.slow_kind = ORC_SLOW_STENCIL;
+    cfg.S = S; cfg.R = R; cfg.rho = rho;
+    cfg.species = species; cfg.reactions = reactions; cfg.rspecies = rspecies;
+    cfg.order = order; cfg.diffusion = diffusion; cfg.vel_kind = 0;
+    cfg.u_const[0] = cfg.u_const[1] = cfg.u_const[2] = 1.0;
+    cfg.threads = 1;
+    cfg.imex = imex ? 1 : 0;
+    cfg.d_impl = imex ? d_impl : 0.0;
+    cfg.cg_iters = cg_iters;
+    orc_sys* cs = orc_sys_create(&cfg);
+    PartitionedSystem sysC;
+    sysC.dimension = dof;
+    if (fast)
+      sysC.f_fast = [cs](double t, const StateVector& y) {
+        StateVector o(y.size());
+        orc_sys_fast_rhs(cs, t, y.data(), o.data());
+        return o;
+      };
+    sysC.f_explicit = [cs](double t, const StateVector& y) {
+      StateVector o(y.size());
+      orc_sys_slow_rhs(cs, t, y.data(), o.data());
+      return o;
+    };
+    if (imex) {
+      sysC.f_implicit = [cs](double t, const StateVector& y) {
+        StateVector o(y.size());
+        orc_sys_implicit_rhs(cs, t, y.data(), o.data());
+        return o;
+      };
+      sysC.jv_implicit = [cs](double t, const StateVector&, const StateVector& v) {
+        StateVector o(v.size());
+        orc_sys_implicit_rhs(cs, t, v.data(), o.data());
+        return o;
+      };
+    }
+    StateVector yB, yC;
+    EvalCounters cB, cC;
+    if (which == 0) {
+      yB = b200::reference_solution(dev, y0, 0.0, steps * h, h);
+      yC = reference_solution(sysC, y0, 0.0, steps * h, h);
+    } else {
+      ImplicitStageSolver solver;
+      if (newton) {
+        solver.newton.tolerance = newton[0];
+        solver.newton.safety = newton[1];
+        solver.newton.max_iters = (int)newton[2];
+      }
+      if (weights) {
+        solver.weights = StateVector(dof);
+        std::memcpy(solver.weights.data(), weights, dof * sizeof(double));
+      }
+      double ymax = 0.0;
+      for (double v : y0) ymax = std::max(ymax, std::fabs(v));
+      solver.gmres.tolerance = 1e-15 * (1.0 + ymax);
+      solver.gmres.safety = 1.0;
+      solver.gmres.max_iters = 200;
+      const ArkPair pair = lookup_ark_pair("ark436-imex-pair");
+      yB = b200::ark_imex_integrate(dev, solver, 0.0, steps * h, h, y0, cB);
+      yC = ark_imex_integrate(pair, sysC, solver, 0.0, steps * h, h, y0, cC);
+    }
+    orc_sys_destroy(cs);
+    errs[0] = rel_err(yB, yC, ncomp);
+    b200::to_c(cB, counters);
+    b200::to_c(cC, counters + 8);
+    return 0;
+  } catch (const std::exception& e) {
+    if (err && errlen) std::snprintf(err, errlen, "%s", e.what());
+    return 1;
+  }
+}

@@ -72,3 +72,34 @@ def test_facade_imex_modes_agree():
     assert errs.max() <= 1e-10, errs
     assert np.array_equal(cnt[8:16], cnt[16:24])  # same reference stepper both sides
     assert solver_counts_ok(cnt[0:8], cnt[16:24], 8)
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="facade test library not built (needs the reference)")
+@pytest.mark.parametrize("which", [0, 1])
+def test_facade_refsol_and_ark(which):
+    """b200::reference_solution / b200::ark_imex_integrate vs the reference's
+    reference_solution / ark_imex_integrate on the CPU physics."""
+    L = C.CDLL(LIB)
+    cfg = dict(CONFIGS["C5"])
+    S, R, n = cfg["S"], cfg["R"], 8
+    sp, rx, rs = P.mechanism(cfg["mech_seed"], S, R)
+    y0 = P.initial_condition(cfg["ic_seed"], S, cfg["rho"], sp, n, n, n)
+    tol, safety, mx, w = stage_solver(y0)
+    newton = np.array([tol, safety, mx], dtype=np.float64)
+    weights = np.ascontiguousarray(w)
+    errs = np.zeros(1)
+    cnt = np.zeros(16, dtype=np.uint64)
+    err = C.create_string_buffer(512)
+    dp = C.POINTER(C.c_double)
+    h, steps = (2e-17, 4) if which == 0 else (2e-3, 2)
+    rc = L.facade_selftest2(
+        C.c_int(which), C.c_int(n), C.c_int(S), C.c_int(R), C.c_double(cfg["rho"]),
+        sp.ctypes.data_as(dp), rx.ctypes.data_as(dp), rs.ctypes.data_as(C.POINTER(C.c_int)),
+        y0.ctypes.data_as(dp), C.c_int(8), C.c_double(0.0), C.c_double(0.05), C.c_int(8),
+        C.c_int(1 if which == 0 else 0), C.c_double(h), C.c_int(steps),
+        newton.ctypes.data_as(dp), weights.ctypes.data_as(dp), errs.ctypes.data_as(dp),
+        cnt.ctypes.data_as(C.POINTER(C.c_uint64)), err, C.c_size_t(512))
+    assert rc == 0, err.value.decode()
+    assert errs[0] <= 1e-10 * steps, errs
+    if which == 1:
+        assert solver_counts_ok(cnt[0:8], cnt[8:16], 8)
