@@ -213,8 +213,6 @@ uint64_t mr_launch_count(const mr_ctx* ctx);
 double mr_chem_flops_per_eval(const mr_ctx* ctx);
 /* measured fp64 FMA peak of this GPU (DFMA chain microbenchmark), TFLOP/s */
 int mr_fp64_peak(mr_ctx* ctx, double* tflops);
-/* enable/disable CUDA-graph replay of the slow step (default on) */
-int mr_set_graphs(mr_ctx* ctx, int enable);
 /* record CUDA events around every launch class of a step (default off) */
 int mr_set_profiling(mr_ctx* ctx, int enable);
 /* per-kernel-class device time of the last step (ms), from CUDA events */

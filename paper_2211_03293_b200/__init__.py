@@ -128,7 +128,6 @@ def lib():
         "mr_launch_count": (C.c_uint64, [vp]),
         "mr_chem_flops_per_eval": (C.c_double, [vp]),
         "mr_fp64_peak": (C.c_int, [vp, _dp]),
-        "mr_set_graphs": (C.c_int, [vp, C.c_int]),
         "mr_set_profiling": (C.c_int, [vp, C.c_int]),
         "mr_last_step_profile": (C.c_int, [vp, _dp, _dp, _dp]),
     }

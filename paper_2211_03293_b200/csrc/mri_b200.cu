@@ -217,7 +217,6 @@ struct mr_ctx {
   double prof_chem = 0, prof_slow = 0, prof_other = 0;
   std::vector<cudaEvent_t> ev_pool;
   int fail_mri = -1, fail_sub = -1, fail_inner = -1;
-  bool graphs = true;
 };
 
 namespace {
@@ -2300,13 +2299,6 @@ int mr_fp64_peak(mr_ctx* c, double* tflops)
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   *tflops = best;
-  return MR_OK;
-}
-
-int mr_set_graphs(mr_ctx* c, int enable)
-{
-  if (!c) return MR_CONTRACT;
-  c->graphs = enable != 0;
   return MR_OK;
 }
 
