@@ -8,6 +8,7 @@
 // (oracle/mri_oracle.c sten_range); HBM-bound: 8*ncomp*ncell bytes read and
 // written once per evaluation.
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -226,6 +227,199 @@ __global__ void __launch_bounds__(kTX * kTY, 2) stencil25d_kernel(const StencilA
   }
 }
 
+// ---------------------------------------------------------------------------
+// K2 v2: 2.5D march along axis 0 with a cp.async ring of whole plane tiles
+// (interior 16 x 64 + halos, M + PF + 1 slots).  Loads in flight live in
+// shared memory, not registers; each thread owns two adjacent axis-2 points,
+// keeps their axis-0 register queues and reads in-plane neighbours as
+// conflict-free LDS.128 pairs (axis 2: one window of 2M+2 values per row
+// serves both outputs).  Same per-point formula and term order as
+// stencil25d_kernel.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* dst, const void* src)
+{
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src)
+{
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+#ifndef MR_V2_TJ
+#define MR_V2_TJ 8
+#endif
+constexpr int kV2TJ = MR_V2_TJ, kV2TK = 64, kV2PF = 3, kV2Threads = 32 * MR_V2_TJ;
+template <int M>
+constexpr size_t v2_smem_bytes()
+{
+  return (size_t)(M + kV2PF + 1) * (kV2TJ + 2 * M) * (kV2TK + 2 * M) * sizeof(double);  // R slots
+}
+
+template <int M>
+__global__ void __launch_bounds__(kV2Threads, (kV2Threads <= 256 ? 2 : 1)) stencil_v2_kernel(const StencilArgs a, int iper)
+{
+  constexpr int PF = kV2PF;
+  constexpr int RJ = kV2TJ + 2 * M, RK = kV2TK + 2 * M, R = M + PF + 1;
+  extern __shared__ __align__(16) double ring[];  // [R][RJ][RK]
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int k0 = blockIdx.x * kV2TK, j0 = blockIdx.y * kV2TJ;
+  const int nchunk = (a.n0l + iper - 1) / iper;
+  const int comp = blockIdx.z / nchunk;
+  const int ib = (blockIdx.z % nchunk) * iper;
+  const int ie = min(a.n0l, ib + iper);
+  const int n0l = a.n0l, n1 = a.n1, n2 = a.n2;
+  const size_t plane = (size_t)n1 * n2;
+  const size_t ncell = plane * n0l;
+  const double* __restrict__ y = a.y + (size_t)comp * ncell;
+  const double* blo = a.halo_lo + (size_t)comp * M * plane + (ptrdiff_t)M * (ptrdiff_t)plane;
+  const double* bhi = a.halo_hi + (size_t)comp * M * plane - (ptrdiff_t)n0l * (ptrdiff_t)plane;
+  auto plane_ptr = [&](int ip) -> const double* {
+    const double* b = ip < 0 ? blo : y;
+    b = ip >= n0l ? bhi : b;
+    return b + (ptrdiff_t)ip * (ptrdiff_t)plane;
+  };
+  auto slot = [&](int ip) -> double* { return ring + (size_t)((unsigned)(ip - ib) % R) * RJ * RK; };
+  // this thread's copy chunks of a plane tile, fixed for the whole march:
+  // 16-B chunks for even M (8-B for M = 1); offsets precomputed once
+  constexpr int CW = (M % 2 == 0) ? 2 : 1;          // doubles per chunk
+  constexpr int CPR = RK / CW;                      // chunks per row
+  constexpr int NCH = (RJ * CPR + kV2Threads - 1) / kV2Threads;
+  int coff_src[NCH], coff_dst[NCH];
+#pragma unroll
+  for (int u = 0; u < NCH; ++u) {
+    const int c = tid + u * kV2Threads;
+    coff_dst[u] = -1;
+    if (c < RJ * CPR) {
+      const int r = c / CPR, cc = c - r * CPR;
+      const int jr = (j0 - M + r + n1) % n1;
+      const int kr = (k0 - M + CW * cc + n2) % n2;
+      coff_src[u] = jr * n2 + kr;
+      coff_dst[u] = r * RK + CW * cc;
+    }
+  }
+  auto issue = [&](int ip) {
+    if (ip < ie + M) {
+      const double* src = plane_ptr(ip);
+      double* dst = slot(ip);
+#pragma unroll
+      for (int u = 0; u < NCH; ++u) {
+        if (coff_dst[u] < 0) continue;
+        if constexpr (CW == 2) cp_async16(dst + coff_dst[u], src + coff_src[u]);
+        else cp_async8(dst + coff_dst[u], src + coff_src[u]);
+      }
+    }
+    cp_async_commit();
+  };
+  auto pair = [&](const double* t, int r, int c, double& v0, double& v1) {
+    if constexpr (M % 2 == 0) {
+      const double2 v = *reinterpret_cast<const double2*>(t + r * RK + c);
+      v0 = v.x;
+      v1 = v.y;
+    } else {
+      v0 = t[r * RK + c];
+      v1 = t[r * RK + c + 1];
+    }
+  };
+
+  // this thread's points: row jl, columns kl, kl+1 of the tile
+  const int jl = ty + M, kl = 2 * tx + M;
+  const int jg = j0 + ty, kA = k0 + 2 * tx;
+  double cdif[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) cdif[d] = a.D * a.inv_dx2[d];
+  const double* P = a.prof;
+  const int nm = a.nmax;
+  double cadv0[2];  // u_0 depends on (j, k): constant along the march
+#pragma unroll
+  for (int e = 0; e < 2; ++e)
+    cadv0[e] = (a.vel_kind == 0 ? a.u[0] : P[(0 * 2 + 0) * nm + jg] + P[(0 * 2 + 1) * nm + kA + e]) *
+               a.inv_dx[0];
+
+  // prologue: planes ib .. ib+M+PF-1 into the ring (one commit group each);
+  // the queue's planes ib-M .. ib-1 straight from global memory.  The axis-0
+  // queue is circular: plane p lives in slot (p - ib + M) % Q, and the march
+  // is unrolled by Q so every slot index is a compile-time constant (no
+  // register shuffling per plane).
+  constexpr int Q = 2 * M + 1;
+  for (int q = 0; q < M + PF; ++q) issue(ib + q);
+  double q0[Q], q1[Q];
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    const double* src = plane_ptr(ib - M + q) + (size_t)jg * n2 + kA;
+    q0[q] = __ldg(src);
+    q1[q] = __ldg(src + 1);
+  }
+  cp_async_wait<PF>();  // planes ib .. ib+M-1 (own copies) ...
+  __syncthreads();      // ... and everyone's
+#pragma unroll
+  for (int q = M; q < 2 * M; ++q) pair(slot(ib - M + q), jl, kl, q0[q], q1[q]);
+
+  const int nplanes = ie - ib;
+  for (int t0 = 0; t0 < nplanes; t0 += Q) {
+#pragma unroll
+    for (int ph = 0; ph < Q; ++ph) {
+      const int t = t0 + ph;
+      if (t >= nplanes) break;
+      const int i = ib + t;
+      cp_async_wait<PF - 1>();  // plane i+M landed (own copies) ...
+      __syncthreads();          // ... and everyone's; plane i-1's slot is free again
+      issue(i + M + PF);
+      pair(slot(i + M), jl, kl, q0[(ph + 2 * M) % Q], q1[(ph + 2 * M) % Q]);
+      const double* tc = slot(i);
+      const int ig = a.i0 + i;
+      double cadv1[2], cadv2;  // u_1 depends on (i, k), u_2 on (i, j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        cadv1[e] = (a.vel_kind == 0 ? a.u[1] : P[(1 * 2 + 0) * nm + ig] + P[(1 * 2 + 1) * nm + kA + e]) *
+                   a.inv_dx[1];
+      cadv2 = (a.vel_kind == 0 ? a.u[2] : P[(2 * 2 + 0) * nm + ig] + P[(2 * 2 + 1) * nm + jg]) *
+              a.inv_dx[2];
+      // axis-2 window of the row: columns kl-M .. kl+1+M
+      double w[2 * M + 2];
+#pragma unroll
+      for (int c = 0; c < M + 1; ++c) pair(tc, jl, kl - M + 2 * c, w[2 * c], w[2 * c + 1]);
+      const int cq = (ph + M) % Q;
+      double acc0 = (cdif[0] + cdif[1] + cdif[2]) * a.b[0] * q0[cq];
+      double acc1 = (cdif[0] + cdif[1] + cdif[2]) * a.b[0] * q1[cq];
+#pragma unroll
+      for (int m = 1; m <= M; ++m) {
+        const int qp = (ph + M + m) % Q, qm = (ph + M - m) % Q;
+        double up0, up1, dn0, dn1;  // axis 1: rows jl + m, jl - m
+        pair(tc, jl + m, kl, up0, up1);
+        pair(tc, jl - m, kl, dn0, dn1);
+        const double bp0 = cdif[0] * a.b[m], bp1 = cdif[1] * a.b[m], bp2 = cdif[2] * a.b[m];
+        const double ap2 = cadv2 * a.a[m];
+        {
+          const double ap0 = cadv0[0] * a.a[m], ap1 = cadv1[0] * a.a[m];
+          acc0 = fma(bp0 - ap0, q0[qp], acc0);
+          acc0 = fma(bp0 + ap0, q0[qm], acc0);
+          acc0 = fma(bp1 - ap1, up0, acc0);
+          acc0 = fma(bp1 + ap1, dn0, acc0);
+          acc0 = fma(bp2 - ap2, w[M + m], acc0);
+          acc0 = fma(bp2 + ap2, w[M - m], acc0);
+        }
+        {
+          const double ap0 = cadv0[1] * a.a[m], ap1 = cadv1[1] * a.a[m];
+          acc1 = fma(bp0 - ap0, q1[qp], acc1);
+          acc1 = fma(bp0 + ap0, q1[qm], acc1);
+          acc1 = fma(bp1 - ap1, up1, acc1);
+          acc1 = fma(bp1 + ap1, dn1, acc1);
+          acc1 = fma(bp2 - ap2, w[M + 1 + m], acc1);
+          acc1 = fma(bp2 + ap2, w[M + 1 - m], acc1);
+        }
+      }
+      double* o = a.out + (size_t)comp * ncell + (size_t)i * plane + (size_t)jg * n2 + kA;
+      *reinterpret_cast<double2*>(o) = make_double2(acc0, acc1);
+    }
+  }
+  cp_async_wait<0>();
+}
+
 // halo planes: send_lo = first g planes, send_hi = last g planes, per component
 __global__ void halo_pack_kernel(const double* __restrict__ y, double* __restrict__ send_lo,
                                  double* __restrict__ send_hi, int ncomp, int n0l, size_t plane,
@@ -289,7 +483,7 @@ __global__ void __launch_bounds__(256) slow_linear_kernel(const double* __restri
 
 // ---------------- K4 reductions (fixed-order two-pass) ----------------
 constexpr int kRedThreads = 256;
-constexpr int kRedBlocks = 592;  // 4 x 148 SMs; fixed so results are run-to-run bitwise
+constexpr int kRedBlocks = 1184;  // 8 x 148 SMs; fixed so results are run-to-run bitwise
 
 __device__ __forceinline__ double red_op(int kind, double a, double b)
 {
@@ -297,31 +491,42 @@ __device__ __forceinline__ double red_op(int kind, double a, double b)
   return a + b;
 }
 
-__global__ void __launch_bounds__(kRedThreads) reduce_partial(int kind, const double* __restrict__ x,
+template <int KIND>
+__device__ __forceinline__ double red_term(const double* __restrict__ x,
+                                           const double* __restrict__ w, size_t i)
+{
+  const double v = x[i];
+  if (KIND == RED_WRMS) { const double xw = v * w[i]; return xw * xw; }
+  if (KIND == RED_TWO) return v * v;
+  if (KIND == RED_DOT) return v * w[i];
+  if (KIND == RED_MAX) return fabs(v);
+  return isfinite(v) ? 0.0 : 1.0;
+}
+
+// grid-stride over a fixed grid, four independent accumulators (loads in
+// flight), combined in a fixed order: deterministic for a given n
+template <int KIND>
+__global__ void __launch_bounds__(kRedThreads) reduce_partial(const double* __restrict__ x,
                                                              const double* __restrict__ w, size_t n,
                                                              double* __restrict__ part)
 {
-  double acc = 0.0;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const double v = x[i];
-    double t;
-    switch (kind) {
-      case RED_WRMS: { const double xw = v * w[i]; t = xw * xw; break; }
-      case RED_TWO: t = v * v; break;
-      case RED_DOT: t = v * w[i]; break;
-      case RED_MAX: t = fabs(v); break;
-      default: t = isfinite(v) ? 0.0 : 1.0; break;
-    }
-    acc = red_op(kind == RED_NONFINITE ? RED_TWO : kind, acc, t);
+  constexpr int OP = KIND == RED_NONFINITE ? RED_TWO : KIND;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    a0 = red_op(OP, a0, red_term<KIND>(x, w, i));
+    a1 = red_op(OP, a1, red_term<KIND>(x, w, i + stride));
+    a2 = red_op(OP, a2, red_term<KIND>(x, w, i + 2 * stride));
+    a3 = red_op(OP, a3, red_term<KIND>(x, w, i + 3 * stride));
   }
+  for (; i < n; i += stride) a0 = red_op(OP, a0, red_term<KIND>(x, w, i));
+  const double acc = red_op(OP, red_op(OP, a0, a1), red_op(OP, a2, a3));
   __shared__ double sh[kRedThreads];
   sh[threadIdx.x] = acc;
   __syncthreads();
   for (int o = kRedThreads / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o)
-      sh[threadIdx.x] = red_op(kind == RED_NONFINITE ? RED_TWO : kind, sh[threadIdx.x],
-                               sh[threadIdx.x + o]);
+    if (threadIdx.x < o) sh[threadIdx.x] = red_op(OP, sh[threadIdx.x], sh[threadIdx.x + o]);
     __syncthreads();
   }
   if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
@@ -369,6 +574,28 @@ __global__ void fp64_peak_kernel(double* sink, int iters)
 cudaError_t launch_stencil(const StencilArgs& a, cudaStream_t st)
 {
   const size_t ncell = (size_t)a.n0l * a.n1 * a.n2;
+  static const bool v2 = getenv("MR_STENCIL_V1") == nullptr;  // A/B hook
+  if (v2 && a.n1 % kV2TJ == 0 && a.n2 % kV2TK == 0) {
+    const size_t tiles = (size_t)(a.n1 / kV2TJ) * (a.n2 / kV2TK) * a.ncomp;
+    int iper = a.n0l;
+    while (iper > 16 && tiles * ((a.n0l + iper - 1) / iper) < 148 * 8) iper = (iper + 1) / 2;
+    const unsigned nch = (unsigned)((a.n0l + iper - 1) / iper);
+    dim3 grid(a.n2 / kV2TK, a.n1 / kV2TJ, (unsigned)a.ncomp * nch);
+    dim3 block(32, kV2Threads / 32);
+    cudaError_t e = cudaSuccess;
+    if (a.M == 1) {
+      cudaFuncSetAttribute(stencil_v2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v2_smem_bytes<1>());
+      stencil_v2_kernel<1><<<grid, block, v2_smem_bytes<1>(), st>>>(a, iper);
+    } else if (a.M == 2) {
+      cudaFuncSetAttribute(stencil_v2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v2_smem_bytes<2>());
+      stencil_v2_kernel<2><<<grid, block, v2_smem_bytes<2>(), st>>>(a, iper);
+    } else {
+      cudaFuncSetAttribute(stencil_v2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v2_smem_bytes<4>());
+      stencil_v2_kernel<4><<<grid, block, v2_smem_bytes<4>(), st>>>(a, iper);
+    }
+    (void)e;
+    return cudaGetLastError();
+  }
   if (a.n1 % kTY == 0 && a.n2 % kTX == 0 && a.n1 >= kTY && a.n2 >= kTX) {
     // planes per block: enough blocks to fill 148 SMs several times over
     const size_t tiles = (size_t)(a.n1 / kTY) * (a.n2 / kTX) * a.ncomp;
@@ -431,7 +658,13 @@ int reduce_blocks() { return kRedBlocks; }
 cudaError_t launch_reduce(int kind, const double* x, const double* w, size_t n, double* d_part,
                           int nblocks, double* d_out, cudaStream_t st)
 {
-  reduce_partial<<<nblocks, kRedThreads, 0, st>>>(kind, x, w, n, d_part);
+  switch (kind) {
+    case RED_WRMS: reduce_partial<RED_WRMS><<<nblocks, kRedThreads, 0, st>>>(x, w, n, d_part); break;
+    case RED_TWO: reduce_partial<RED_TWO><<<nblocks, kRedThreads, 0, st>>>(x, w, n, d_part); break;
+    case RED_DOT: reduce_partial<RED_DOT><<<nblocks, kRedThreads, 0, st>>>(x, w, n, d_part); break;
+    case RED_MAX: reduce_partial<RED_MAX><<<nblocks, kRedThreads, 0, st>>>(x, w, n, d_part); break;
+    default: reduce_partial<RED_NONFINITE><<<nblocks, kRedThreads, 0, st>>>(x, w, n, d_part); break;
+  }
   reduce_final<<<1, 1024, 0, st>>>(kind, d_part, nblocks, n, d_out);
   return cudaGetLastError();
 }
@@ -453,35 +686,22 @@ cudaError_t launch_fp64_peak(double* sink, int blocks, int threads, int iters, c
 namespace {
 
 constexpr int kLapThreads = 256;
-constexpr int kLapBlocks = 592;
+constexpr int kLapBlocks = 1184;  // fixed grid: the dot-product partials are deterministic
 
-__device__ __forceinline__ double lap7_at(const LapArgs& a, const double* __restrict__ y,
-                                          const double* lo, const double* hi, size_t comp,
-                                          size_t cell)
+// 7-point Laplacian of one element given its row pointers (same operation
+// order as the oracle, no contraction)
+__device__ __forceinline__ double lap7_row(const LapArgs& a, const double* __restrict__ row,
+                                           const double* __restrict__ rowp0,
+                                           const double* __restrict__ rowm0,
+                                           const double* __restrict__ rowp1,
+                                           const double* __restrict__ rowm1, int k)
 {
-  const size_t plane = (size_t)a.n1 * a.n2;
-  const int i = (int)(cell / plane);
-  const size_t rem = cell - (size_t)i * plane;
-  const int j = (int)(rem / a.n2);
-  const int k = (int)(rem - (size_t)j * a.n2);
-  const size_t ncell = plane * a.n0l;
-  const double* yc = y + comp * ncell;
-  const double c0 = yc[cell];
-  // axis 0 through the halo planes (nearest: lo plane M-1, hi plane 0)
-  const double* lo_c = lo + comp * (size_t)a.M * plane;
-  const double* hi_c = hi + comp * (size_t)a.M * plane;
-  const double yp0 = i + 1 < a.n0l ? yc[cell + plane] : hi_c[rem];
-  const double ym0 = i > 0 ? yc[cell - plane] : lo_c[(size_t)(a.M - 1) * plane + rem];
-  const int jp = j + 1 < a.n1 ? j + 1 : 0, jm = j > 0 ? j - 1 : a.n1 - 1;
   const int kp = k + 1 < a.n2 ? k + 1 : 0, km = k > 0 ? k - 1 : a.n2 - 1;
-  const size_t base = (size_t)i * plane;
-  const double yp1 = yc[base + (size_t)jp * a.n2 + k], ym1 = yc[base + (size_t)jm * a.n2 + k];
-  const double yp2 = yc[base + (size_t)j * a.n2 + kp], ym2 = yc[base + (size_t)j * a.n2 + km];
-  // same operation order as the oracle, no contraction
+  const double c0 = row[k];
   const double c2 = dmul(2.0, c0);
-  double lap = dmul(dadd(dadd(yp0, ym0), -c2), a.inv_dx2[0]);
-  lap = dadd(lap, dmul(dadd(dadd(yp1, ym1), -c2), a.inv_dx2[1]));
-  lap = dadd(lap, dmul(dadd(dadd(yp2, ym2), -c2), a.inv_dx2[2]));
+  double lap = dmul(dadd(dadd(rowp0[k], rowm0[k]), -c2), a.inv_dx2[0]);
+  lap = dadd(lap, dmul(dadd(dadd(rowp1[k], rowm1[k]), -c2), a.inv_dx2[1]));
+  lap = dadd(lap, dmul(dadd(dadd(row[kp], row[km]), -c2), a.inv_dx2[2]));
   return dmul(a.D, lap);
 }
 
@@ -503,6 +723,9 @@ __device__ __forceinline__ void block_sum_store(double v, double* part)
 //         G = (Y - gamma D L7 Y) - known; r = -G; z = r/dg; p = z;
 //         partials sum (G w)^2 -> part, r.z -> part2
 // MODE 2: q = p - gamma D L7 p; partial p.q -> part        (CG matvec, y = p)
+// Rows (comp, i, j) are distributed over a fixed grid of blocks and the
+// threads of a block walk the row along axis 2 (coalesced; k +- 1 from L1,
+// j +- 1 rows and the i +- 1 planes from L1/L2): no per-element division.
 template <int MODE>
 __global__ void __launch_bounds__(kLapThreads) lap7_kernel(const LapArgs a, const double* y,
                                                            const double* lo, const double* hi,
@@ -510,31 +733,50 @@ __global__ void __launch_bounds__(kLapThreads) lap7_kernel(const LapArgs a, cons
                                                            double* o1, double* o2, double* o3,
                                                            double* part, double* part2)
 {
-  const size_t ncell = (size_t)a.n0l * a.n1 * a.n2;
-  const size_t n = ncell * a.ncomp;
+  const size_t plane = (size_t)a.n1 * a.n2;
+  const size_t ncell = plane * a.n0l;
+  const long nrows = (long)a.ncomp * a.n0l * a.n1;
   double acc = 0.0, acc2 = 0.0;
-  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const size_t comp = idx / ncell, cell = idx - comp * ncell;
-    const double f = lap7_at(a, y, lo, hi, comp, cell);
-    if (MODE == 0) {
-      o1[idx] = f;
-    } else if (MODE == 1) {
-      double G = dadd(y[idx], dmul(-a.gamma, f));
-      G = dadd(G, dmul(-1.0, known[idx]));
-      const double r = -G;
-      const double z = r / a.dg;
-      o1[idx] = r;
-      o2[idx] = z;
-      o3[idx] = z;
-      const double Gw = w ? dmul(G, w[idx]) : G;
-      acc = dadd(acc, dmul(Gw, Gw));
-      acc2 = dadd(acc2, dmul(r, z));
-    } else {
-      const double pv = y[idx];
-      const double q = dadd(pv, -dmul(a.gamma, f));
-      o1[idx] = q;
-      acc = dadd(acc, dmul(pv, q));
+  for (long r = blockIdx.x; r < nrows; r += gridDim.x) {
+    const int j = (int)(r % a.n1);
+    const long ci = r / a.n1;
+    const int i = (int)(ci % a.n0l);
+    const int comp = (int)(ci / a.n0l);
+    const double* yc = y + (size_t)comp * ncell;
+    const double* lo_c = lo + (size_t)comp * a.M * plane;
+    const double* hi_c = hi + (size_t)comp * a.M * plane;
+    const size_t jrow = (size_t)j * a.n2;
+    const size_t base = (size_t)i * plane + jrow;
+    const double* row = yc + base;
+    // axis 0 through the halo planes (nearest: lo plane M-1, hi plane 0)
+    const double* rowp0 = i + 1 < a.n0l ? row + plane : hi_c + jrow;
+    const double* rowm0 = i > 0 ? row - plane : lo_c + (size_t)(a.M - 1) * plane + jrow;
+    const int jp = j + 1 < a.n1 ? j + 1 : 0, jm = j > 0 ? j - 1 : a.n1 - 1;
+    const double* rowp1 = yc + (size_t)i * plane + (size_t)jp * a.n2;
+    const double* rowm1 = yc + (size_t)i * plane + (size_t)jm * a.n2;
+    const size_t obase = (size_t)comp * ncell + base;
+    for (int k = threadIdx.x; k < a.n2; k += blockDim.x) {
+      const double f = lap7_row(a, row, rowp0, rowm0, rowp1, rowm1, k);
+      const size_t idx = obase + k;
+      if (MODE == 0) {
+        o1[idx] = f;
+      } else if (MODE == 1) {
+        double G = dadd(row[k], dmul(-a.gamma, f));
+        G = dadd(G, dmul(-1.0, known[idx]));
+        const double rr = -G;
+        const double z = rr / a.dg;
+        o1[idx] = rr;
+        o2[idx] = z;
+        o3[idx] = z;
+        const double Gw = w ? dmul(G, w[idx]) : G;
+        acc = dadd(acc, dmul(Gw, Gw));
+        acc2 = dadd(acc2, dmul(rr, z));
+      } else {
+        const double pv = row[k];
+        const double q = dadd(pv, -dmul(a.gamma, f));
+        o1[idx] = q;
+        acc = dadd(acc, dmul(pv, q));
+      }
     }
   }
   if (MODE != 0) block_sum_store(acc, part);
@@ -542,6 +784,7 @@ __global__ void __launch_bounds__(kLapThreads) lap7_kernel(const LapArgs a, cons
 }
 
 // Y += alpha p; r -= alpha q; z = r/dg; partial r.z  (alpha = pAp != 0 ? rz/pAp : 0)
+// double2 accesses (all buffers are cudaMalloc-aligned; an odd tail is done last)
 __global__ void __launch_bounds__(kLapThreads) cg_update_kernel(size_t n, double dg,
                                                                 const double* sc, double* Y,
                                                                 double* r, double* z,
@@ -551,8 +794,23 @@ __global__ void __launch_bounds__(kLapThreads) cg_update_kernel(size_t n, double
   const double rz = sc[0], pAp = sc[1];
   const double alpha = pAp != 0.0 ? rz / pAp : 0.0;
   double acc = 0.0;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x) {
+  const size_t n2 = n / 2, stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n2; v += stride) {
+    const double2 Yv = reinterpret_cast<const double2*>(Y)[v];
+    const double2 pv = reinterpret_cast<const double2*>(p)[v];
+    const double2 rv = reinterpret_cast<const double2*>(r)[v];
+    const double2 qv = reinterpret_cast<const double2*>(q)[v];
+    const double r0 = dadd(rv.x, -dmul(alpha, qv.x)), r1 = dadd(rv.y, -dmul(alpha, qv.y));
+    const double z0 = r0 / dg, z1 = r1 / dg;
+    reinterpret_cast<double2*>(Y)[v] =
+        make_double2(dadd(Yv.x, dmul(alpha, pv.x)), dadd(Yv.y, dmul(alpha, pv.y)));
+    reinterpret_cast<double2*>(r)[v] = make_double2(r0, r1);
+    reinterpret_cast<double2*>(z)[v] = make_double2(z0, z1);
+    acc = dadd(acc, dmul(r0, z0));
+    acc = dadd(acc, dmul(r1, z1));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const size_t i = n - 1;
     Y[i] = dadd(Y[i], dmul(alpha, p[i]));
     const double rr = dadd(r[i], -dmul(alpha, q[i]));
     const double zz = rr / dg;
@@ -569,9 +827,14 @@ __global__ void __launch_bounds__(kLapThreads) cg_p_kernel(size_t n, const doubl
 {
   const double rz = sc[0], rzn = sc[2];
   const double beta = rz != 0.0 ? rzn / rz : 0.0;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x)
-    p[i] = dadd(z[i], dmul(beta, p[i]));
+  const size_t n2 = n / 2, stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n2; v += stride) {
+    const double2 zv = reinterpret_cast<const double2*>(z)[v];
+    const double2 pv = reinterpret_cast<const double2*>(p)[v];
+    reinterpret_cast<double2*>(p)[v] =
+        make_double2(dadd(zv.x, dmul(beta, pv.x)), dadd(zv.y, dmul(beta, pv.y)));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[n - 1] = dadd(z[n - 1], dmul(beta, p[n - 1]));
 }
 
 // fixed-order sum of the block partials into sc[slot]
@@ -619,10 +882,17 @@ __global__ void __launch_bounds__(256) recover_fi_kernel(size_t n, double gamma,
                                                          int mri_stage, unsigned long long* fail)
 {
   bool bad = false;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const double y = Y[i];
-    fI[i] = dadd(y, -known[i]) / gamma;
+  const size_t n2 = n / 2, stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n2; v += stride) {
+    const double2 y = reinterpret_cast<const double2*>(Y)[v];
+    const double2 kn = reinterpret_cast<const double2*>(known)[v];
+    reinterpret_cast<double2*>(fI)[v] =
+        make_double2(dadd(y.x, -kn.x) / gamma, dadd(y.y, -kn.y) / gamma);
+    bad |= !isfinite(y.x) || !isfinite(y.y);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const double y = Y[n - 1];
+    fI[n - 1] = dadd(y, -known[n - 1]) / gamma;
     bad |= !isfinite(y);
   }
   if (bad) atomicMin(fail, mr_fail_key(mri_stage, 0, 1));

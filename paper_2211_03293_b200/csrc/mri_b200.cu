@@ -2258,6 +2258,66 @@ int mr_step_counts(const char* text, int s_f, int m, int fast_present, int slow_
 }
 
 // ---------------- instrumentation ----------------
+// Debug (not part of include/mri_b200.h): HBM throughput of the vector
+// kernels (K3 update, sum/add combines, K5 IMEX kernels, K4 reductions) on
+// this context's state-sized buffers.  out[2*q] = ms per launch, out[2*q+1] =
+// algorithmic GB/s; returns the number of kernels measured.
+int mr_debug_vector_bench(mr_ctx* c, double* out, int maxn)
+{
+  if (!c || !c->has_grid || c->slow_kind != SK_STENCIL) return -1;
+  cudaSetDevice(c->device);
+  if (ensure_state(c) || ensure_slots(c, 3) || ensure_cg(c) || ensure_halo(c)) return -1;
+  cudaStream_t st = c->stream;
+  const size_t n = c->dof;
+  const double B = 8.0 * (double)n;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int q = 0;
+  auto timeit = [&](double bytes, auto&& launch) {
+    launch();
+    cudaEventRecord(e0, st);
+    const int reps = 5;
+    for (int r = 0; r < reps; ++r) launch();
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (q < maxn) {
+      out[2 * q] = ms / reps;
+      out[2 * q + 1] = bytes / (ms / reps * 1e-3) / 1e9;
+    }
+    ++q;
+  };
+  double* y = c->y_state;
+  double* o = c->y_work;
+  double** sl = c->slots.data();
+  const double* f3[3] = {sl[0], sl[1], sl[2]};
+  const double cf3[3] = {1e-3, 2e-3, 3e-3};
+  cudaMemsetAsync(c->d_fail, 0xFF, sizeof(unsigned long long), st);
+  timeit(3 * B, [&] { launch_update(y, o, 1, f3, cf3, n, 0, c->d_fail, st); });
+  timeit(5 * B, [&] { launch_update(y, o, 3, f3, cf3, n, 0, c->d_fail, st); });
+  timeit(4 * B, [&] { launch_sum_rhs(n, sl[0], sl[1], sl[2], o, st); });
+  const double* lo = c->send_hi;
+  const double* hi = c->send_lo;
+  launch_halo_pack(y, c->send_lo, c->send_hi, c->ncomp, c->n0l, c->plane, c->M, st);
+  LapArgs la = lap_args(c, 1e-3);
+  timeit(2 * B, [&] { launch_lap7(0, la, y, lo, hi, nullptr, nullptr, o, nullptr, nullptr, nullptr, nullptr, st); });
+  timeit(5 * B, [&] { launch_lap7(1, la, y, lo, hi, c->cg_known, nullptr, c->cg_r, c->cg_z, c->cg_p, c->cg_part, c->cg_part2, st); });
+  timeit(2 * B, [&] { launch_lap7(2, la, c->cg_p, lo, hi, nullptr, nullptr, c->cg_q, nullptr, nullptr, c->cg_part, nullptr, st); });
+  cudaMemsetAsync(c->cg_sc, 0, 8 * sizeof(double), st);
+  timeit(7 * B, [&] { launch_cg_update(n, la.dg, c->cg_sc, o, c->cg_r, c->cg_z, c->cg_p, c->cg_q, c->cg_part, st); });
+  timeit(3 * B, [&] { launch_cg_p(n, c->cg_sc, c->cg_p, c->cg_z, st); });
+  timeit(3 * B, [&] { launch_recover_fi(n, 1.0, o, c->cg_known, c->cg_q, 0, c->d_fail, st); });
+  const int nb = reduce_blocks();
+  timeit(2 * B, [&] { launch_reduce(RED_WRMS, y, o, n, c->d_red, nb, c->d_red + nb, st); });
+  timeit(2 * B, [&] { launch_reduce(RED_DOT, y, o, n, c->d_red, nb, c->d_red + nb, st); });
+  timeit(1 * B, [&] { launch_reduce(RED_MAX, y, nullptr, n, c->d_red, nb, c->d_red + nb, st); });
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return q;
+}
+
 // Debug (not part of include/mri_b200.h): chemistry phase cycles of an
 // MR_PHASE_PROF build, summed over blocks; out[7] = blocks.  reset zeroes them.
 int mr_debug_chem_phases(mr_ctx* c, uint64_t* out, int reset)

@@ -1,7 +1,10 @@
 """Chemistry-kernel phase breakdown (needs an MR_PHASE_PROF build selected by
 MR_LIB_PATH).  Usage: MR_LIB_PATH=variants/prof/libmri_b200.so python scripts/phase_prof.py [CONFIG] [N]"""
 import ctypes as C
+import os
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import numpy as np
 

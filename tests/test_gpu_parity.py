@@ -63,9 +63,10 @@ def test_slow_rhs_matches_oracle(name):
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3"])
-def test_slow_rhs_tiled_kernel_matches_oracle(name):
-    """n1 % 8 == 0 and n2 % 32 == 0 selects the 2.5D shared-memory stencil."""
-    n = 32
+@pytest.mark.parametrize("n", [32, 64])
+def test_slow_rhs_tiled_kernel_matches_oracle(name, n):
+    """n1 % 8 == 0 and n2 % 32 == 0 selects the 2.5D register-queue stencil;
+    n1 % 16 == 0 and n2 % 64 == 0 the cp.async-ring version (orders 2/4/8)."""
     ctx, cfg, y0 = gpu_ctx(name, n)
     ref = oracle_physics(cfg, n).slow_rhs(y0)
     got = ctx.slow_rhs(y0)
@@ -338,7 +339,7 @@ def test_reductions_match_reference_definitions():
 
 
 # ------------------------------------------------------------- slabs
-@pytest.mark.parametrize("P_,n", [(2, 16), (4, 16), (4, 32), (3, 32)])
+@pytest.mark.parametrize("P_,n", [(2, 16), (4, 16), (4, 32), (3, 32), (3, 64)])
 def test_virtual_rank_slabs_equal_single_gpu_bitwise(P_, n):
     """Slab decomposition (8th-order halos of 4 planes) on in-process virtual
     ranks reproduces the single-slab result bit-for-bit (n = 32 exercises the
