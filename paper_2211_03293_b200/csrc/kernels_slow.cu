@@ -420,6 +420,198 @@ __global__ void __launch_bounds__(kV2Threads, (kV2Threads <= 256 ? 2 : 1)) stenc
   cp_async_wait<0>();
 }
 
+constexpr int kV3TJ = 16, kV3PF = 4;  // measured: PF 2/3/4/6 -> 45/46/51/40% of HBM at 256^3
+template <int M>
+constexpr size_t v3_smem_bytes()
+{
+  return (size_t)(M + kV3PF + 1) * (kV3TJ + 2 * M) * (kV2TK + 2 * M) * sizeof(double);
+}
+
+// K2 v3 (order 8): as v2 with a 2 x 2 register block per thread (rows jl,
+// jl+1) -- the axis-1 rows jl - m and jl + 1 + m each serve two outputs per
+// column pair, cutting the shared wavefronts per point by ~30% -- one
+// 256-thread block per SM (251 registers) and a 4-plane prefetch.
+template <int M>
+__global__ void __launch_bounds__(256, 1) stencil_v3_kernel(const StencilArgs a, int iper)
+{
+  constexpr int PF = kV3PF;
+  constexpr int RJ = kV3TJ + 2 * M, RK = kV2TK + 2 * M, R = M + PF + 1;
+  constexpr int kThreads = 256;
+  extern __shared__ __align__(16) double ring[];  // [R][RJ][RK]
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int k0 = blockIdx.x * kV2TK, j0 = blockIdx.y * kV3TJ;
+  const int nchunk = (a.n0l + iper - 1) / iper;
+  const int comp = blockIdx.z / nchunk;
+  const int ib = (blockIdx.z % nchunk) * iper;
+  const int ie = min(a.n0l, ib + iper);
+  const int n0l = a.n0l, n1 = a.n1, n2 = a.n2;
+  const size_t plane = (size_t)n1 * n2;
+  const size_t ncell = plane * n0l;
+  const double* __restrict__ y = a.y + (size_t)comp * ncell;
+  const double* blo = a.halo_lo + (size_t)comp * M * plane + (ptrdiff_t)M * (ptrdiff_t)plane;
+  const double* bhi = a.halo_hi + (size_t)comp * M * plane - (ptrdiff_t)n0l * (ptrdiff_t)plane;
+  auto plane_ptr = [&](int ip) -> const double* {
+    const double* b = ip < 0 ? blo : y;
+    b = ip >= n0l ? bhi : b;
+    return b + (ptrdiff_t)ip * (ptrdiff_t)plane;
+  };
+  auto slot = [&](int ip) -> double* { return ring + (size_t)((unsigned)(ip - ib) % R) * RJ * RK; };
+  // this thread's copy chunks of a plane tile, fixed for the whole march:
+  // 16-B chunks for even M (8-B for M = 1); offsets precomputed once
+  constexpr int CW = (M % 2 == 0) ? 2 : 1;          // doubles per chunk
+  constexpr int CPR = RK / CW;                      // chunks per row
+  constexpr int NCH = (RJ * CPR + kThreads - 1) / kThreads;
+  int coff_src[NCH], coff_dst[NCH];
+#pragma unroll
+  for (int u = 0; u < NCH; ++u) {
+    const int c = tid + u * kThreads;
+    coff_dst[u] = -1;
+    if (c < RJ * CPR) {
+      const int r = c / CPR, cc = c - r * CPR;
+      const int jr = (j0 - M + r + n1) % n1;
+      const int kr = (k0 - M + CW * cc + n2) % n2;
+      coff_src[u] = jr * n2 + kr;
+      coff_dst[u] = r * RK + CW * cc;
+    }
+  }
+  auto issue = [&](int ip) {
+    if (ip < ie + M) {
+      const double* src = plane_ptr(ip);
+      double* dst = slot(ip);
+#pragma unroll
+      for (int u = 0; u < NCH; ++u) {
+        if (coff_dst[u] < 0) continue;
+        if constexpr (CW == 2) cp_async16(dst + coff_dst[u], src + coff_src[u]);
+        else cp_async8(dst + coff_dst[u], src + coff_src[u]);
+      }
+    }
+    cp_async_commit();
+  };
+  auto pair = [&](const double* t, int r, int c, double& v0, double& v1) {
+    if constexpr (M % 2 == 0) {
+      const double2 v = *reinterpret_cast<const double2*>(t + r * RK + c);
+      v0 = v.x;
+      v1 = v.y;
+    } else {
+      v0 = t[r * RK + c];
+      v1 = t[r * RK + c + 1];
+    }
+  };
+
+  // this thread's 2 x 2 points: rows jl, jl+1 and columns kl, kl+1 of the tile
+  const int jl = 2 * ty + M, kl = 2 * tx + M;
+  const int jA = j0 + 2 * ty, kA = k0 + 2 * tx;
+  double cdif[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) cdif[d] = a.D * a.inv_dx2[d];
+  const double* P = a.prof;
+  const int nm = a.nmax;
+  double cadv0[4];  // u_0 depends on (j, k): constant along the march
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+    cadv0[p] = (a.vel_kind == 0 ? a.u[0]
+                                : P[(0 * 2 + 0) * nm + jA + (p >> 1)] + P[(0 * 2 + 1) * nm + kA + (p & 1)]) *
+               a.inv_dx[0];
+
+  constexpr int Q = 2 * M + 1;
+  for (int q = 0; q < M + PF; ++q) issue(ib + q);
+  double qv[4][Q];
+#pragma unroll
+  for (int q = 0; q < M; ++q)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const double* src = plane_ptr(ib - M + q) + (size_t)(jA + e) * n2 + kA;
+      qv[2 * e][q] = __ldg(src);
+      qv[2 * e + 1][q] = __ldg(src + 1);
+    }
+  cp_async_wait<PF>();
+  __syncthreads();
+#pragma unroll
+  for (int q = M; q < 2 * M; ++q)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) pair(slot(ib - M + q), jl + e, kl, qv[2 * e][q], qv[2 * e + 1][q]);
+
+  const int nplanes = ie - ib;
+  for (int t0 = 0; t0 < nplanes; t0 += Q) {
+#pragma unroll
+    for (int ph = 0; ph < Q; ++ph) {
+      const int t = t0 + ph;
+      if (t >= nplanes) break;
+      const int i = ib + t;
+      cp_async_wait<PF - 1>();
+      __syncthreads();
+      issue(i + M + PF);
+      const double* tq = slot(i + M);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) pair(tq, jl + e, kl, qv[2 * e][(ph + 2 * M) % Q], qv[2 * e + 1][(ph + 2 * M) % Q]);
+      const double* tc = slot(i);
+      const int ig = a.i0 + i;
+      double cadv1[2], cadv2[2];  // u_1 depends on (i, k), u_2 on (i, j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        cadv1[e] = (a.vel_kind == 0 ? a.u[1] : P[(1 * 2 + 0) * nm + ig] + P[(1 * 2 + 1) * nm + kA + e]) *
+                   a.inv_dx[1];
+        cadv2[e] = (a.vel_kind == 0 ? a.u[2] : P[(2 * 2 + 0) * nm + ig] + P[(2 * 2 + 1) * nm + jA + e]) *
+                   a.inv_dx[2];
+      }
+      const int cq = (ph + M) % Q;
+      double acc[4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) acc[p] = (cdif[0] + cdif[1] + cdif[2]) * a.b[0] * qv[p][cq];
+      // axis 0 (register queue) and axis 2 (row windows), row by row
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double w[2 * M + 2];
+#pragma unroll
+        for (int c = 0; c < M + 1; ++c) pair(tc, jl + e, kl - M + 2 * c, w[2 * c], w[2 * c + 1]);
+#pragma unroll
+        for (int m = 1; m <= M; ++m) {
+          const int qp = (ph + M + m) % Q, qm = (ph + M - m) % Q;
+          const double bp0 = cdif[0] * a.b[m], bp2 = cdif[2] * a.b[m];
+          const double ap2 = cadv2[e] * a.a[m];
+#pragma unroll
+          for (int pk = 0; pk < 2; ++pk) {
+            const int p = 2 * e + pk;
+            const double ap0 = cadv0[p] * a.a[m];
+            acc[p] = fma(bp0 - ap0, qv[p][qp], acc[p]);
+            acc[p] = fma(bp0 + ap0, qv[p][qm], acc[p]);
+            acc[p] = fma(bp2 - ap2, w[M + pk + m], acc[p]);
+            acc[p] = fma(bp2 + ap2, w[M + pk - m], acc[p]);
+          }
+        }
+      }
+      // axis 1: rows jl - m and jl + 1 + m are loaded once and serve both rows
+      double pu0 = qv[2][cq], pu1 = qv[3][cq];  // row jl + 1 (for m = 1: row jl + m)
+      double pd0 = qv[0][cq], pd1 = qv[1][cq];  // row jl     (for m = 1: row jl + 1 - m)
+#pragma unroll
+      for (int m = 1; m <= M; ++m) {
+        double up0, up1, dn0, dn1;
+        pair(tc, jl + 1 + m, kl, up0, up1);
+        pair(tc, jl - m, kl, dn0, dn1);
+        const double bp1 = cdif[1] * a.b[m];
+#pragma unroll
+        for (int pk = 0; pk < 2; ++pk) {
+          const double ap1 = cadv1[pk] * a.a[m];
+          // row jl: y(j + m) = row jl + m (previous "up"), y(j - m) = row jl - m
+          acc[pk] = fma(bp1 - ap1, pk ? pu1 : pu0, acc[pk]);
+          acc[pk] = fma(bp1 + ap1, pk ? dn1 : dn0, acc[pk]);
+          // row jl + 1: y(j + 1 + m) = row jl + 1 + m, y(j + 1 - m) = row jl + 1 - m (previous "dn")
+          acc[2 + pk] = fma(bp1 - ap1, pk ? up1 : up0, acc[2 + pk]);
+          acc[2 + pk] = fma(bp1 + ap1, pk ? pd1 : pd0, acc[2 + pk]);
+        }
+        pu0 = up0; pu1 = up1;
+        pd0 = dn0; pd1 = dn1;
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double* o = a.out + (size_t)comp * ncell + (size_t)i * plane + (size_t)(jA + e) * n2 + kA;
+        *reinterpret_cast<double2*>(o) = make_double2(acc[2 * e], acc[2 * e + 1]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
 // halo planes: send_lo = first g planes, send_hi = last g planes, per component
 __global__ void halo_pack_kernel(const double* __restrict__ y, double* __restrict__ send_lo,
                                  double* __restrict__ send_hi, int ncomp, int n0l, size_t plane,
@@ -575,6 +767,25 @@ cudaError_t launch_stencil(const StencilArgs& a, cudaStream_t st)
 {
   const size_t ncell = (size_t)a.n0l * a.n1 * a.n2;
   static const bool v2 = getenv("MR_STENCIL_V1") == nullptr;  // A/B hook
+  if (v2 && a.M == 4 && a.n1 % kV3TJ == 0 && a.n2 % kV2TK == 0) {
+    const size_t tiles = (size_t)(a.n1 / kV3TJ) * (a.n2 / kV2TK) * a.ncomp;
+    int iper = a.n0l;
+    while (iper > 16 && tiles * ((a.n0l + iper - 1) / iper) < 148 * 8) iper = (iper + 1) / 2;
+    const unsigned nch = (unsigned)((a.n0l + iper - 1) / iper);
+    dim3 grid(a.n2 / kV2TK, a.n1 / kV3TJ, (unsigned)a.ncomp * nch);
+    dim3 block(32, 8);
+    if (a.M == 1) {
+      cudaFuncSetAttribute(stencil_v3_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3_smem_bytes<1>());
+      stencil_v3_kernel<1><<<grid, block, v3_smem_bytes<1>(), st>>>(a, iper);
+    } else if (a.M == 2) {
+      cudaFuncSetAttribute(stencil_v3_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3_smem_bytes<2>());
+      stencil_v3_kernel<2><<<grid, block, v3_smem_bytes<2>(), st>>>(a, iper);
+    } else {
+      cudaFuncSetAttribute(stencil_v3_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3_smem_bytes<4>());
+      stencil_v3_kernel<4><<<grid, block, v3_smem_bytes<4>(), st>>>(a, iper);
+    }
+    return cudaGetLastError();
+  }
   if (v2 && a.n1 % kV2TJ == 0 && a.n2 % kV2TK == 0) {
     const size_t tiles = (size_t)(a.n1 / kV2TJ) * (a.n2 / kV2TK) * a.ncomp;
     int iper = a.n0l;
