@@ -994,6 +994,133 @@ __global__ void __launch_bounds__(kLapThreads) lap7_kernel(const LapArgs a, cons
   if (MODE == 1) block_sum_store(acc2, part2);
 }
 
+// Tiled version for the production grids (n1 % 8 == 0, n2 % 64 == 0): the
+// same per-element arithmetic, with every plane tile (8 x 64 + halos) brought
+// in once by cp.async into a ring of PF + 3 slots and all seven neighbours read
+// from shared memory.  A fixed grid of blocks walks (component, tile, plane
+// run) work items, so the dot-product partials stay deterministic.
+constexpr int kLTJ = 8, kLTK = 64, kLPF = 3;
+constexpr int kLRJ = kLTJ + 2, kLRK = kLTK + 4, kLR = kLPF + 3;
+constexpr size_t lap7_tile_smem() { return (size_t)kLR * kLRJ * kLRK * sizeof(double); }
+
+template <int MODE>
+__global__ void __launch_bounds__(256) lap7_tile_kernel(const LapArgs a, const double* y,
+                                                        const double* lo, const double* hi,
+                                                        const double* known, const double* w,
+                                                        double* o1, double* o2, double* o3,
+                                                        double* part, double* part2)
+{
+  extern __shared__ __align__(16) double ring[];  // [kLR][kLRJ][kLRK]
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, tid = threadIdx.x;
+  const int n0l = a.n0l, n1 = a.n1, n2 = a.n2;
+  const size_t plane = (size_t)n1 * n2, ncell = plane * n0l;
+  const int nk = n2 / kLTK, nj = n1 / kLTJ;
+  const long ntiles = (long)nk * nj * a.ncomp;
+  const int jl = ty + 1, kl = 2 * tx + 2;
+  double acc = 0.0, acc2 = 0.0;
+  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int kt = (int)(tile % nk);
+    const long r1 = tile / nk;
+    const int jt = (int)(r1 % nj);
+    const int comp = (int)(r1 / nj);
+    const int k0 = kt * kLTK, j0 = jt * kLTJ;
+    const double* yc = y + (size_t)comp * ncell;
+    const double* loc = lo + ((size_t)comp * a.M + (a.M - 1)) * plane;  // nearest lower halo plane
+    const double* hic = hi + (size_t)comp * a.M * plane;                 // nearest upper halo plane
+    auto plane_ptr = [&](int ip) -> const double* {
+      return ip < 0 ? loc : (ip >= n0l ? hic : yc + (size_t)ip * plane);
+    };
+    // this thread's 16-B chunks of a tile (rows j0-1 .. j0+8, columns k0-2 .. k0+65)
+    constexpr int CPR = kLRK / 2, NCH = (kLRJ * CPR + 255) / 256;
+    int cs[NCH], cd[NCH];
+#pragma unroll
+    for (int u = 0; u < NCH; ++u) {
+      const int c = tid + u * 256;
+      cd[u] = -1;
+      if (c < kLRJ * CPR) {
+        const int r = c / CPR, cc = c - r * CPR;
+        const int jr = (j0 - 1 + r + n1) % n1;
+        const int kr = (k0 - 2 + 2 * cc + n2) % n2;
+        cs[u] = jr * n2 + kr;
+        cd[u] = r * kLRK + 2 * cc;
+      }
+    }
+    auto slot = [&](int ip) -> double* { return ring + (size_t)((unsigned)(ip + 1) % kLR) * kLRJ * kLRK; };
+    auto issue = [&](int ip) {
+      if (ip <= n0l) {
+        const double* src = plane_ptr(ip);
+        double* dst = slot(ip);
+#pragma unroll
+        for (int u = 0; u < NCH; ++u)
+          if (cd[u] >= 0) cp_async16(dst + cd[u], src + cs[u]);
+      }
+      cp_async_commit();
+    };
+    for (int q = -1; q <= kLPF; ++q) issue(q);
+    for (int i = 0; i < n0l; ++i) {
+      cp_async_wait<kLPF - 1>();  // plane i+1 landed
+      __syncthreads();
+      issue(i + kLPF + 1);        // into the slot of plane i-2
+      const double* tm = slot(i - 1) + jl * kLRK + kl;
+      const double* tc = slot(i) + jl * kLRK + kl;
+      const double* tp = slot(i + 1) + jl * kLRK + kl;
+      const double2 c = *reinterpret_cast<const double2*>(tc);
+      const double2 xm = *reinterpret_cast<const double2*>(tm);
+      const double2 xp = *reinterpret_cast<const double2*>(tp);
+      const double2 up = *reinterpret_cast<const double2*>(tc + kLRK);
+      const double2 dn = *reinterpret_cast<const double2*>(tc - kLRK);
+      const double2 lf = *reinterpret_cast<const double2*>(tc - 2);
+      const double2 rt = *reinterpret_cast<const double2*>(tc + 2);
+      double f[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double c0 = e ? c.y : c.x;
+        const double c2 = dmul(2.0, c0);
+        const double km = e ? c.x : lf.y, kp = e ? rt.x : c.y;
+        double lap = dmul(dadd(dadd(e ? xp.y : xp.x, e ? xm.y : xm.x), -c2), a.inv_dx2[0]);
+        lap = dadd(lap, dmul(dadd(dadd(e ? up.y : up.x, e ? dn.y : dn.x), -c2), a.inv_dx2[1]));
+        lap = dadd(lap, dmul(dadd(dadd(kp, km), -c2), a.inv_dx2[2]));
+        f[e] = dmul(a.D, lap);
+      }
+      const size_t idx = (size_t)comp * ncell + (size_t)i * plane + (size_t)(j0 + ty) * n2 + k0 + 2 * tx;
+      if (MODE == 0) {
+        *reinterpret_cast<double2*>(o1 + idx) = make_double2(f[0], f[1]);
+      } else if (MODE == 1) {
+        const double2 kn = *reinterpret_cast<const double2*>(known + idx);
+        double2 wv = make_double2(1.0, 1.0);
+        if (w) wv = *reinterpret_cast<const double2*>(w + idx);
+        double rr[2], zz[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double G = dadd(e ? c.y : c.x, dmul(-a.gamma, f[e]));
+          G = dadd(G, dmul(-1.0, e ? kn.y : kn.x));
+          rr[e] = -G;
+          zz[e] = rr[e] / a.dg;
+          const double Gw = w ? dmul(G, e ? wv.y : wv.x) : G;
+          acc = dadd(acc, dmul(Gw, Gw));
+          acc2 = dadd(acc2, dmul(rr[e], zz[e]));
+        }
+        *reinterpret_cast<double2*>(o1 + idx) = make_double2(rr[0], rr[1]);
+        *reinterpret_cast<double2*>(o2 + idx) = make_double2(zz[0], zz[1]);
+        *reinterpret_cast<double2*>(o3 + idx) = make_double2(zz[0], zz[1]);
+      } else {
+        double q[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double pv = e ? c.y : c.x;
+          q[e] = dadd(pv, -dmul(a.gamma, f[e]));
+          acc = dadd(acc, dmul(pv, q[e]));
+        }
+        *reinterpret_cast<double2*>(o1 + idx) = make_double2(q[0], q[1]);
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // the ring is reused by the next work item
+  }
+  if (MODE != 0) block_sum_store(acc, part);
+  if (MODE == 1) block_sum_store(acc2, part2);
+}
+
 // Y += alpha p; r -= alpha q; z = r/dg; partial r.z  (alpha = pAp != 0 ? rz/pAp : 0)
 // double2 accesses (all buffers are cudaMalloc-aligned; an odd tail is done last)
 __global__ void __launch_bounds__(kLapThreads) cg_update_kernel(size_t n, double dg,
@@ -1145,6 +1272,21 @@ cudaError_t launch_lap7(int mode, const LapArgs& a, const double* y, const doubl
                         const double* hi, const double* known, const double* w, double* o1,
                         double* o2, double* o3, double* part, double* part2, cudaStream_t st)
 {
+  static const bool tiled = getenv("MR_LAP7_ROWS") == nullptr;  // A/B hook
+  if (tiled && a.n1 % kLTJ == 0 && a.n2 % kLTK == 0) {
+    const size_t sm = lap7_tile_smem();
+    if (mode == 0) {
+      cudaFuncSetAttribute(lap7_tile_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      lap7_tile_kernel<0><<<kLapBlocks, 256, sm, st>>>(a, y, lo, hi, known, w, o1, o2, o3, part, part2);
+    } else if (mode == 1) {
+      cudaFuncSetAttribute(lap7_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      lap7_tile_kernel<1><<<kLapBlocks, 256, sm, st>>>(a, y, lo, hi, known, w, o1, o2, o3, part, part2);
+    } else {
+      cudaFuncSetAttribute(lap7_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      lap7_tile_kernel<2><<<kLapBlocks, 256, sm, st>>>(a, y, lo, hi, known, w, o1, o2, o3, part, part2);
+    }
+    return cudaGetLastError();
+  }
   if (mode == 0)
     lap7_kernel<0><<<kLapBlocks, kLapThreads, 0, st>>>(a, y, lo, hi, known, w, o1, o2, o3, part, part2);
   else if (mode == 1)

@@ -208,3 +208,21 @@ def test_ark_imex_failures():
     P.setup_workload(ctx2, "C4", n=8)
     with pytest.raises(P.ContractError):
         ctx2.ark_imex_step(0.0, 1e-17)
+
+
+def test_tiled_laplacian_paths_match_oracle():
+    """n1 % 8 == 0 and n2 % 64 == 0 select the tiled 7-point kernels (f_I
+    evaluation, Newton residual, CG matvec): one IMEX step with active PCG
+    on 64^3 against the oracle, plus f_I itself."""
+    n = 64
+    cfg0 = c5(d_impl=0.05, cg_iters=4, m=2)
+    ctx, cfg, y0 = gpu_case(n, cfg0, fast=False)
+    sysm = oracle_system(cfg, n, fast="none", y0=y0)
+    sysm.set_threads(os.cpu_count() or 1)
+    assert per_species_rel_err(ctx.implicit_rhs(y0), sysm.implicit_rhs(y0), cfg["S"] + 1) <= 1e-12
+    H = 2e-4
+    y_ref, cnt_ref = sysm.mri_step(GARK3B, "kutta3", 2, 0.0, H, y0)
+    cnt = ctx.mri_step(0.0, H)
+    assert np.array_equal(cnt, cnt_ref)
+    assert cnt[4] > 0  # Newton iterated: residual + PCG kernels ran
+    assert per_species_rel_err(ctx.download(), y_ref, cfg["S"] + 1) <= 1e-12
