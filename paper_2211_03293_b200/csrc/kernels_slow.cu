@@ -420,7 +420,11 @@ __global__ void __launch_bounds__(kV2Threads, (kV2Threads <= 256 ? 2 : 1)) stenc
   cp_async_wait<0>();
 }
 
-constexpr int kV3TJ = 16, kV3PF = 4;  // measured: PF 2/3/4/6 -> 45/46/51/40% of HBM at 256^3
+#ifndef MR_V3_TJ
+#define MR_V3_TJ 16
+#endif
+constexpr int kV3TJ = MR_V3_TJ, kV3PF = 4;  // measured: PF 2/3/4/6 -> 45/46/51/40% of HBM at 256^3
+constexpr int kV3Threads = 16 * kV3TJ;      // 2 x 2 points per thread
 template <int M>
 constexpr size_t v3_smem_bytes()
 {
@@ -432,11 +436,11 @@ constexpr size_t v3_smem_bytes()
 // column pair, cutting the shared wavefronts per point by ~30% -- one
 // 256-thread block per SM (251 registers) and a 4-plane prefetch.
 template <int M>
-__global__ void __launch_bounds__(256, 1) stencil_v3_kernel(const StencilArgs a, int iper)
+__global__ void __launch_bounds__(kV3Threads, 256 / kV3Threads) stencil_v3_kernel(const StencilArgs a, int iper)
 {
   constexpr int PF = kV3PF;
   constexpr int RJ = kV3TJ + 2 * M, RK = kV2TK + 2 * M, R = M + PF + 1;
-  constexpr int kThreads = 256;
+  constexpr int kThreads = kV3Threads;
   extern __shared__ __align__(16) double ring[];  // [R][RJ][RK]
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
   const int k0 = blockIdx.x * kV2TK, j0 = blockIdx.y * kV3TJ;
@@ -773,7 +777,7 @@ cudaError_t launch_stencil(const StencilArgs& a, cudaStream_t st)
     while (iper > 16 && tiles * ((a.n0l + iper - 1) / iper) < 148 * 8) iper = (iper + 1) / 2;
     const unsigned nch = (unsigned)((a.n0l + iper - 1) / iper);
     dim3 grid(a.n2 / kV2TK, a.n1 / kV3TJ, (unsigned)a.ncomp * nch);
-    dim3 block(32, 8);
+    dim3 block(32, kV3TJ / 2);
     if (a.M == 1) {
       cudaFuncSetAttribute(stencil_v3_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3_smem_bytes<1>());
       stencil_v3_kernel<1><<<grid, block, v3_smem_bytes<1>(), st>>>(a, iper);
