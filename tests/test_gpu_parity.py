@@ -53,6 +53,48 @@ def test_fast_rhs_matches_oracle(name):
     assert np.all(got[S * 512:] == 0.0)  # de/dt = 0
 
 
+@pytest.mark.parametrize("S,R", [(63, 200), (30, 800), (12, 600), (4, 1)])
+def test_fast_rhs_mechanism_sizes(S, R):
+    """Mechanism-size edges of the chemistry kernel: the largest species count
+    (S + 1 = 64 slots), rate buffers split into several shared-memory chunks
+    (R = 800, 1000), the smallest mechanism; RK steps with them too."""
+    n = 8
+    cfg = dict(CONFIGS["C3"], S=S, R=R, mech_seed=777 + S + R)
+    ctx = P.Context(0)
+    cfg, y0 = P.setup_workload(ctx, "C3", n=n, config=cfg)
+    ref = oracle_physics(cfg, n).fast_rhs(y0)
+    got = ctx.fast_rhs(y0)
+    assert per_species_rel_err(got[: S * n ** 3], ref[: S * n ** 3], S) <= RHS_TOL
+    assert np.all(got[S * n ** 3:] == 0.0)
+    # one slow step (fast IVPs with this mechanism) against the oracle
+    sysm = oracle_physics(cfg, n)
+    H = 1e-17
+    ctx.method(cfg["coupling"], cfg["fast_table"], 4)
+    try:
+        y_ref, cnt_ref = sysm.mri_step(P.coupling_text(cfg["coupling"]), cfg["fast_table"], 4,
+                                       0.0, H, y0)
+    except O.StepError as eo:  # a stiff synthetic mechanism may blow up: same failure
+        cnt = ctx.counters()
+        with pytest.raises(P.IntegrationError) as eg:
+            ctx.mri_step(0.0, H, cnt)
+        assert eg.value.stage_index == eo.stage
+        assert np.array_equal(cnt, eo.counters)
+        assert np.array_equal(ctx.download(), y0)
+        return
+    cnt = ctx.mri_step(0.0, H)
+    assert np.array_equal(cnt, cnt_ref)
+    assert per_species_rel_err(ctx.download(), y_ref, S + 1) <= STEP_TOL
+
+
+def test_mechanism_over_shared_memory_is_contract_error():
+    """A mechanism whose reaction records cannot be staged in shared memory
+    is refused up front (no silent slow path)."""
+    cfg = dict(CONFIGS["C3"], S=12, R=1000, mech_seed=5)
+    ctx = P.Context(0)
+    with pytest.raises(P.ContractError, match="shared memory"):
+        P.setup_workload(ctx, "C3", n=8, config=cfg)
+
+
 @pytest.mark.parametrize("name", ["C1", "C2", "C3"])
 def test_slow_rhs_matches_oracle(name):
     n = 12
