@@ -478,10 +478,9 @@ __global__ void __launch_bounds__(kV3Threads, 256 / kV3Threads) stencil_v3_kerne
       coff_dst[u] = r * RK + CW * cc;
     }
   }
-  auto issue = [&](int ip) {
+  auto issue_to = [&](int ip, double* dst) {
     if (ip < ie + M) {
       const double* src = plane_ptr(ip);
-      double* dst = slot(ip);
 #pragma unroll
       for (int u = 0; u < NCH; ++u) {
         if (coff_dst[u] < 0) continue;
@@ -491,6 +490,7 @@ __global__ void __launch_bounds__(kV3Threads, 256 / kV3Threads) stencil_v3_kerne
     }
     cp_async_commit();
   };
+  auto issue = [&](int ip) { issue_to(ip, slot(ip)); };
   auto pair = [&](const double* t, int r, int c, double& v0, double& v1) {
     if constexpr (M % 2 == 0) {
       const double2 v = *reinterpret_cast<const double2*>(t + r * RK + c);
@@ -544,11 +544,18 @@ __global__ void __launch_bounds__(kV3Threads, 256 / kV3Threads) stencil_v3_kerne
       const int i = ib + t;
       cp_async_wait<PF - 1>();
       __syncthreads();
-      issue(i + M + PF);
-      const double* tq = slot(i + M);
+      // ring slots: compile-time when the ring and the register queue have the
+      // same period (R == Q, t0 a multiple of Q)
+#ifndef MR_V3_CSLOT
+#define MR_V3_CSLOT 1
+#endif
+      constexpr bool kCs = MR_V3_CSLOT && R == Q;
+      double* const s_iss = kCs ? ring + (size_t)((ph + M + PF) % R) * RJ * RK : slot(i + M + PF);
+      const double* const tq = kCs ? ring + (size_t)((ph + M) % R) * RJ * RK : slot(i + M);
+      const double* const tc = kCs ? ring + (size_t)(ph % R) * RJ * RK : slot(i);
+      issue_to(i + M + PF, s_iss);
 #pragma unroll
       for (int e = 0; e < 2; ++e) pair(tq, jl + e, kl, qv[2 * e][(ph + 2 * M) % Q], qv[2 * e + 1][(ph + 2 * M) % Q]);
-      const double* tc = slot(i);
       const int ig = a.i0 + i;
       double cadv1[2], cadv2[2];  // u_1 depends on (i, k), u_2 on (i, j)
 #pragma unroll
@@ -584,8 +591,17 @@ __global__ void __launch_bounds__(kV3Threads, 256 / kV3Threads) stencil_v3_kerne
           }
         }
       }
-      // axis 1: rows jl - m and jl + 1 + m are loaded once and serve both rows
-      double pu0 = qv[2][cq], pu1 = qv[3][cq];  // row jl + 1 (for m = 1: row jl + m)
+      // axis 1: rows jl - m and jl + 1 + m are loaded once and serve both rows;
+      // a second accumulator per point (8 independent DFMA chains per thread)
+#ifndef MR_V3_SPLIT
+#define MR_V3_SPLIT 0  // measured: 2 accumulators per point 4% slower
+#endif
+#if MR_V3_SPLIT
+      double acc1[4] = {0.0, 0.0, 0.0, 0.0};
+#else
+      double (&acc1)[4] = acc;
+#endif
+      double ru0 = qv[2][cq], ru1 = qv[3][cq];  // row jl + 1 (for m = 1: row jl + m)
       double pd0 = qv[0][cq], pd1 = qv[1][cq];  // row jl     (for m = 1: row jl + 1 - m)
 #pragma unroll
       for (int m = 1; m <= M; ++m) {
@@ -597,19 +613,24 @@ __global__ void __launch_bounds__(kV3Threads, 256 / kV3Threads) stencil_v3_kerne
         for (int pk = 0; pk < 2; ++pk) {
           const double ap1 = cadv1[pk] * a.a[m];
           // row jl: y(j + m) = row jl + m (previous "up"), y(j - m) = row jl - m
-          acc[pk] = fma(bp1 - ap1, pk ? pu1 : pu0, acc[pk]);
-          acc[pk] = fma(bp1 + ap1, pk ? dn1 : dn0, acc[pk]);
+          acc1[pk] = fma(bp1 - ap1, pk ? ru1 : ru0, acc1[pk]);
+          acc1[pk] = fma(bp1 + ap1, pk ? dn1 : dn0, acc1[pk]);
           // row jl + 1: y(j + 1 + m) = row jl + 1 + m, y(j + 1 - m) = row jl + 1 - m (previous "dn")
-          acc[2 + pk] = fma(bp1 - ap1, pk ? up1 : up0, acc[2 + pk]);
-          acc[2 + pk] = fma(bp1 + ap1, pk ? pd1 : pd0, acc[2 + pk]);
+          acc1[2 + pk] = fma(bp1 - ap1, pk ? up1 : up0, acc1[2 + pk]);
+          acc1[2 + pk] = fma(bp1 + ap1, pk ? pd1 : pd0, acc1[2 + pk]);
         }
-        pu0 = up0; pu1 = up1;
+        ru0 = up0; ru1 = up1;
         pd0 = dn0; pd1 = dn1;
       }
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         double* o = a.out + (size_t)comp * ncell + (size_t)i * plane + (size_t)(jA + e) * n2 + kA;
-        *reinterpret_cast<double2*>(o) = make_double2(acc[2 * e], acc[2 * e + 1]);
+        *reinterpret_cast<double2*>(o) =
+#if MR_V3_SPLIT
+            make_double2(acc[2 * e] + acc1[2 * e], acc[2 * e + 1] + acc1[2 * e + 1]);
+#else
+            make_double2(acc[2 * e], acc[2 * e + 1]);
+#endif
       }
     }
   }
