@@ -157,6 +157,15 @@ int mr_ark_imex_integrate(mr_ctx* ctx, double t0, double tf, double H, uint64_t*
  * efficiency studies, harness.cpp:411-429).  No counters.  On MR_INTEGRATION
  * the state is unchanged and *fail_stage is erk_step's stage index. */
 int mr_reference_solution(mr_ctx* ctx, double t0, double tf, double h_ref, int* fail_stage);
+/* erk_integrate (proj/src/erk.cpp:40-57) with an explicit table A[s][s]
+ * (row-major), b[s], c[s] (s <= 12) on the summed right-hand side -- the
+ * harness's "erk-<table>" method family (harness.cpp:346-355).  Adds one to
+ * *n_explicit_evals per stage evaluation (erk.cpp:28; may be NULL).  On
+ * MR_INTEGRATION the state is unchanged, *fail_stage is erk_step's stage index
+ * and the count stops where erk_step threw. */
+int mr_erk_integrate(mr_ctx* ctx, int s, const double* A, const double* b, const double* c,
+                     double t0, double tf, double h, uint64_t* n_explicit_evals,
+                     int* fail_stage);
 /* Location of the last failure: MRI stage, fast substep, inner stage. */
 int mr_last_failure(const mr_ctx* ctx, int* mri_stage, int* substep, int* inner_stage);
 

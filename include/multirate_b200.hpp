@@ -205,6 +205,31 @@ inline StateVector reference_solution(Device& d, const StateVector& y0, double t
   return out;
 }
 
+// erk_integrate (erk.cpp:40-57) of f_fast + f_implicit + f_explicit with an
+// explicit table: the harness's "erk-<table>" family (harness.cpp:346-355),
+// counting stage evaluations into *eval_counter like the reference.
+inline StateVector erk_integrate(Device& d, const ButcherTable& table, double t0, double tf,
+                                 double h, const StateVector& y0,
+                                 std::size_t* eval_counter = nullptr)
+{
+  if (y0.size() != d.dof()) throw ContractError("erk_integrate: state size != grid dof");
+  if (table.kind != TableKind::Explicit) throw ContractError("erk_step: table must be explicit");
+  const int s = table.stages;
+  std::vector<double> A(static_cast<size_t>(s) * s);
+  for (int i = 0; i < s; ++i)
+    for (int j = 0; j < s; ++j) A[static_cast<size_t>(i) * s + j] = table.A[i][j];
+  d.check(mr_state_upload(d.ctx(), y0.data()));
+  uint64_t evals = 0;
+  int stage = -1;
+  const int rc = mr_erk_integrate(d.ctx(), s, A.data(), table.b.data(), table.c.data(), t0, tf, h,
+                                  &evals, &stage);
+  if (eval_counter) *eval_counter += static_cast<std::size_t>(evals);
+  d.check(rc, stage);
+  StateVector out(y0.size());
+  d.check(mr_state_download(d.ctx(), out.data()));
+  return out;
+}
+
 // ark_imex_integrate (mri.cpp:542-557) with the ark436 pair
 // (lookup_ark_pair("ark436-imex-pair")) on the device plugins
 inline StateVector ark_imex_integrate(Device& d, const ImplicitStageSolver& solver, double t0,

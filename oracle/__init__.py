@@ -106,6 +106,8 @@ def lib():
                                                  _dp, _u64p, _ip, C.c_char_p, C.c_size_t]
         L.orc_sys_reference_solution.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double,
                                                  _dp, _ip, C.c_char_p, C.c_size_t]
+        L.orc_sys_erk_integrate.argtypes = [C.c_void_p, C.c_char_p, C.c_double, C.c_double,
+                                            C.c_double, _dp, _u64p, _ip, C.c_char_p, C.c_size_t]
         L.orc_sys_mri_integrate.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int,
                                             C.c_double, C.c_double, C.c_double, _dp, _u64p, _ip,
                                             C.c_char_p, C.c_size_t]
@@ -144,6 +146,8 @@ def ref():
                                                  _dp, _u64p, _ip, C.c_char_p, C.c_size_t]
         L.ref_sys_reference_solution.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double,
                                                  _dp, _ip, C.c_char_p, C.c_size_t]
+        L.ref_sys_erk_integrate.argtypes = [C.c_void_p, C.c_char_p, C.c_double, C.c_double,
+                                            C.c_double, _dp, _u64p, _ip, C.c_char_p, C.c_size_t]
         L.ref_sys_mri_integrate.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int,
                                             C.c_double, C.c_double, C.c_double, _dp, _u64p, _ip,
                                             C.c_char_p, C.c_size_t]
@@ -312,6 +316,20 @@ class System:
         if rc:
             raise StepError(rc, stage, err, cnt)
         return y2, cnt
+
+    def erk_integrate(self, table, t0, tf, h, y, use_reference=False):
+        """erk_integrate (erk.cpp:40-57) of the summed RHS with a registered
+        table; returns (y, stage evaluations)."""
+        fn = ref().ref_sys_erk_integrate if use_reference else lib().orc_sys_erk_integrate
+        y2 = np.array(y, dtype=np.float64, copy=True)
+        ev = np.zeros(1, dtype=np.uint64)
+        stage = C.c_int(-1)
+        err = C.create_string_buffer(512)
+        rc = fn(self.h, table.encode(), t0, tf, h, _ptr(y2),
+                ev.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(stage), err, 512)
+        if rc:
+            raise StepError(rc, stage.value, err.value.decode(), ev)
+        return y2, int(ev[0])
 
     def reference_solution(self, t0, tf, h_ref, y, use_reference=False):
         """reference_solution (erk.cpp:59-75): cash-karp5 on the summed RHS."""

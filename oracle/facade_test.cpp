@@ -157,7 +157,8 @@ extern "C" int facade_selftest(int n, int S, int R, double rho, const double* sp
 
 // reference_solution and ark_imex_integrate through the facade (device) vs the
 // reference's own implementations on the CPU physics.  which = 0: reference
-// solution (steps of h); 1: ARK-IMEX (steps of h, IMEX split d_impl).
+// solution (steps of h); 1: ARK-IMEX (steps of h, IMEX split d_impl);
+// 2: erk_integrate with kutta3 (the harness's erk-<table> family).
 extern "C" int facade_selftest2(int which, int n, int S, int R, double rho, const double* species,
                                 const double* reactions, const int* rspecies,
                                 const double* y0in, int order, double diffusion, double d_impl,
@@ -226,6 +227,14 @@ extern "C" int facade_selftest2(int which, int n, int S, int R, double rho, cons
     if (which == 0) {
       yB = b200::reference_solution(dev, y0, 0.0, steps * h, h);
       yC = reference_solution(sysC, y0, 0.0, steps * h, h);
+    } else if (which == 2) {  // erk_integrate (erk.cpp:40-57), kutta3, counted
+      const ButcherTable tb = lookup_table("kutta3");
+      std::size_t eB = 0, eC = 0;
+      yB = b200::erk_integrate(dev, tb, 0.0, steps * h, h, y0, &eB);
+      RhsFn f = [&sysC](double t, const StateVector& v) { return sysC.sum_rhs(t, v); };
+      yC = erk_integrate(tb, f, 0.0, steps * h, h, y0, &eC);
+      cB.n_explicit_evals = eB;
+      cC.n_explicit_evals = eC;
     } else {
       ImplicitStageSolver solver;
       if (newton) {

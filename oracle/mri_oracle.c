@@ -1339,14 +1339,25 @@ static void sum_rhs(const orc_problem* p, double t, const double* y, double* out
 /* reference_solution, proj/src/erk.cpp:59-75: erk_integrate (:40-57) of the
  * registered cash-karp5 table (butcher.cpp:305-321) on sum_rhs; erk_step
  * (:9-38) semantics, no counters.  y is overwritten on success. */
-int orc_reference_solution(const orc_problem* p, double t0, double tf, double h, double* y,
-                           int* fail_stage, char* err, size_t errlen)
+/* erk_integrate (proj/src/erk.cpp:40-57) with erk_step (:9-38) on sum_rhs;
+   *evals (may be NULL) += 1 per stage evaluation (:28) */
+int orc_erk_integrate(const orc_problem* p, const char* table, double t0, double tf, double h,
+                      double* y, uint64_t* evals, int* fail_stage, char* err, size_t errlen)
 {
   *fail_stage = -1;
   if (tf <= t0) { if (err) snprintf(err, errlen, "erk_integrate: tf must exceed t0"); return ORC_CONTRACT; }
   if (h <= 0.0) { if (err) snprintf(err, errlen, "erk_integrate: h must be positive"); return ORC_CONTRACT; }
   orc_table tb;
-  if (orc_table_lookup("cash-karp5", &tb) != ORC_OK) return ORC_CONTRACT;
+  if (orc_table_lookup(table, &tb) != ORC_OK) {
+    if (err) snprintf(err, errlen, "unknown Butcher table '%s'", table);
+    return ORC_CONTRACT;
+  }
+  for (int i = 0; i < tb.s; ++i)
+    for (int j = i; j < tb.s; ++j)
+      if (tb.A[i][j] != 0.0) {
+        if (err) snprintf(err, errlen, "erk_step: table must be explicit");
+        return ORC_CONTRACT;
+      }
   const size_t dof = p->ncell * (size_t)p->ncomp;
   const int s = tb.s;
   double* k[ORC_MAX_TABLE];
@@ -1371,6 +1382,7 @@ int orc_reference_solution(const orc_problem* p, double t0, double tf, double h,
         break;
       }
       sum_rhs(p, t + tb.c[i] * step, stage, k[i], tmp);
+      if (evals) ++*evals;
     }
     if (rc != ORC_OK) break;
     memcpy(stage, work, sizeof(double) * dof);
@@ -1389,6 +1401,13 @@ int orc_reference_solution(const orc_problem* p, double t0, double tf, double h,
   for (int i = 0; i < s; ++i) free(k[i]);
   free(stage); free(tmp); free(work);
   return rc;
+}
+
+/* reference_solution (proj/src/erk.cpp:59-75): cash-karp5 on sum_rhs */
+int orc_reference_solution(const orc_problem* p, double t0, double tf, double h, double* y,
+                           int* fail_stage, char* err, size_t errlen)
+{
+  return orc_erk_integrate(p, "cash-karp5", t0, tf, h, y, NULL, fail_stage, err, errlen);
 }
 
 /* ------------------------------------------------------------------ */
@@ -1533,6 +1552,12 @@ int orc_sys_reference_solution(orc_sys* s, double t0, double tf, double h, doubl
                                int* fail_stage, char* err, size_t errlen)
 {
   return orc_reference_solution(&s->prob, t0, tf, h, y, fail_stage, err, errlen);
+}
+
+int orc_sys_erk_integrate(orc_sys* s, const char* table, double t0, double tf, double h, double* y,
+                          uint64_t* evals, int* fail_stage, char* err, size_t errlen)
+{
+  return orc_erk_integrate(&s->prob, table, t0, tf, h, y, evals, fail_stage, err, errlen);
 }
 
 int orc_sys_ark_imex_integrate(orc_sys* s, double t0, double tf, double H, double* y,

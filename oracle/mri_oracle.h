@@ -227,6 +227,12 @@ int orc_ark_imex_integrate(const orc_problem* p, double t0, double tf, double H,
                            orc_counters* cnt, int* fail_stage, char* err, size_t errlen);
 int orc_sys_ark_imex_integrate(orc_sys* s, double t0, double tf, double H, double* y,
                                uint64_t* counters, int* fail_stage, char* err, size_t errlen);
+/* erk_integrate (proj/src/erk.cpp:40-57) of a named explicit table on sum_rhs;
+   *evals += stage evaluations (erk.cpp:28) */
+int orc_erk_integrate(const orc_problem* p, const char* table, double t0, double tf, double h,
+                      double* y, uint64_t* evals, int* fail_stage, char* err, size_t errlen);
+int orc_sys_erk_integrate(orc_sys* s, const char* table, double t0, double tf, double h, double* y,
+                          uint64_t* evals, int* fail_stage, char* err, size_t errlen);
 /* reference_solution (proj/src/erk.cpp:59-75): cash-karp5 on sum_rhs */
 int orc_reference_solution(const orc_problem* p, double t0, double tf, double h, double* y,
                            int* fail_stage, char* err, size_t errlen);

@@ -283,6 +283,26 @@ extern "C" int ref_sys_reference_solution(orc_sys* sys, double t0, double tf, do
   });
 }
 
+// multirate::erk_integrate (erk.cpp:40-57) of a registered table on sum_rhs,
+// counting into *evals like harness.cpp:353-354
+extern "C" int ref_sys_erk_integrate(orc_sys* sys, const char* table, double t0, double tf,
+                                     double h, double* y, uint64_t* evals, int* fail_stage,
+                                     char* err, size_t errlen)
+{
+  std::size_t cnt = 0;
+  const int rc = guarded(err, errlen, fail_stage, [&] {
+    PartitionedSystem ps = make_system(sys);
+    StateVector yv(ps.dimension);
+    std::memcpy(yv.data(), y, sizeof(double) * ps.dimension);
+    const ButcherTable tb = lookup_table(table);
+    RhsFn f = [&ps](double t, const StateVector& v) { return ps.sum_rhs(t, v); };
+    StateVector out = erk_integrate(tb, f, t0, tf, h, yv, &cnt);
+    std::memcpy(y, out.data(), sizeof(double) * ps.dimension);
+  });
+  *evals += cnt;
+  return rc;
+}
+
 // multirate::ark_imex_integrate (mri.cpp:542-557) with the registered ark436 pair
 extern "C" int ref_sys_ark_imex_integrate(orc_sys* sys, double t0, double tf, double H, double* y,
                                           uint64_t* counters, int* fail_stage, char* err,

@@ -95,6 +95,8 @@ def lib():
         "mr_implicit_rhs": (C.c_int, [vp, C.c_double, _dp, _dp]),
         "mr_newton_config": (C.c_int, [vp, C.c_double, C.c_double, C.c_int, _dp]),
         "mr_reference_solution": (C.c_int, [vp, C.c_double, C.c_double, C.c_double, _ip]),
+        "mr_erk_integrate": (C.c_int, [vp, C.c_int, _dp, _dp, _dp, C.c_double, C.c_double,
+                                       C.c_double, _u64p, _ip]),
         "mr_ark_imex_step": (C.c_int, [vp, C.c_double, C.c_double, _u64p, _ip]),
         "mr_ark_imex_integrate": (C.c_int, [vp, C.c_double, C.c_double, C.c_double, _u64p, _ip]),
         "mr_state_upload": (C.c_int, [vp, _dp]),
@@ -395,6 +397,23 @@ class Context:
         stage = C.c_int(-1)
         rc = self.L.mr_reference_solution(self.h, t0, tf, h_ref, C.byref(stage))
         self._check(rc, stage.value)
+
+    def erk_integrate(self, table, t0, tf, h, counters=None):
+        """erk_integrate (erk.cpp:40-57) of the summed RHS with an explicit table
+        (name or dict): the harness's erk-<table> family.  Stage evaluations are
+        counted into counters[MR_CNT_EXPLICIT_EVALS] like harness.cpp:353-354."""
+        t = tables.lookup_table(table) if isinstance(table, str) else table
+        A = np.ascontiguousarray(t["A"], dtype=np.float64)
+        b = np.ascontiguousarray(t["b"], dtype=np.float64)
+        c = np.ascontiguousarray(t["c"], dtype=np.float64)
+        cnt = self.counters() if counters is None else counters
+        ev = np.zeros(1, dtype=np.uint64)
+        stage = C.c_int(-1)
+        rc = self.L.mr_erk_integrate(self.h, len(b), _p(A), _p(b), _p(c), t0, tf, h,
+                                     _p(ev, _u64p), C.byref(stage))
+        cnt[2] += ev[0]
+        self._check(rc, stage.value)
+        return cnt
 
     def last_failure(self):
         a, b, c = C.c_int(), C.c_int(), C.c_int()

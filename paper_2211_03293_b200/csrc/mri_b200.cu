@@ -1960,10 +1960,13 @@ static int eval_fast_dev(mr_ctx* c, const double* in, double* out)
   return MR_OK;
 }
 
-// reference_solution (erk.cpp:59-75): erk_integrate (:40-57) of cash-karp5
-// (butcher.cpp:305-321) on sum_rhs (partitioned_system.hpp:41-48) over the
-// device-resident state; erk_step's finite checks (:24-36); no counters.
-int mr_reference_solution(mr_ctx* c, double t0, double tf, double h, int* fail_stage)
+// erk_integrate (erk.cpp:40-57) of an explicit table on sum_rhs
+// (partitioned_system.hpp:41-48) over the device-resident state: erk_step's
+// stage loop, finite checks (:24-36) and per-stage evaluation count (:28).
+// On failure the state is restored to its value at entry (the reference's
+// input is const) and the count stops where erk_step threw.
+static int erk_integrate_dev(mr_ctx* c, int s, const double* A, const double* b, double t0,
+                             double tf, double h, uint64_t* evals, int* fail_stage)
 {
   if (fail_stage) *fail_stage = -1;
   if (!c) return MR_CONTRACT;
@@ -1974,25 +1977,17 @@ int mr_reference_solution(mr_ctx* c, double t0, double tf, double h, int* fail_s
     return set_err(c, MR_CONTRACT, "PartitionedSystem: at least one partition required");
   if (!(tf > t0)) return set_err(c, MR_CONTRACT, "erk_integrate: tf must exceed t0");
   if (!(h > 0.0)) return set_err(c, MR_CONTRACT, "erk_integrate: h must be positive");
+  if (s < 1 || s > MR_MAXREF) return set_err(c, MR_CONTRACT, "erk_integrate: 1 <= stages <= 12");
+  for (int i = 0; i < s; ++i)
+    for (int j = i; j < s; ++j)
+      if (A[i * s + j] != 0.0) return set_err(c, MR_CONTRACT, "erk_step: table must be explicit");
   if (c->slow_kind == SK_STENCIL && c->n0l < c->M)
     return set_err(c, MR_CONTRACT, "slab thinner than the stencil ghost width");
   cudaSetDevice(c->device);
   int rc = ensure_state(c);
   if (rc) return rc;
-  // cash-karp5, exactly as butcher.cpp:305-321 writes it
-  const int s = 6;
-  double A[6][6] = {{0}}, b[6] = {0}, cc[6] = {0};
-  A[1][0] = 1.0 / 5.0;
-  A[2][0] = 3.0 / 40.0; A[2][1] = 9.0 / 40.0;
-  A[3][0] = 3.0 / 10.0; A[3][1] = -9.0 / 10.0; A[3][2] = 6.0 / 5.0;
-  A[4][0] = -11.0 / 54.0; A[4][1] = 5.0 / 2.0; A[4][2] = -70.0 / 27.0; A[4][3] = 35.0 / 27.0;
-  A[5][0] = 1631.0 / 55296.0; A[5][1] = 175.0 / 512.0; A[5][2] = 575.0 / 13824.0;
-  A[5][3] = 44275.0 / 110592.0; A[5][4] = 253.0 / 4096.0;
-  b[0] = 37.0 / 378.0; b[2] = 250.0 / 621.0; b[3] = 125.0 / 594.0; b[5] = 512.0 / 1771.0;
-  cc[1] = 1.0 / 5.0; cc[2] = 3.0 / 10.0; cc[3] = 3.0 / 5.0; cc[4] = 1.0; cc[5] = 7.0 / 8.0;
-  (void)cc;
-  // buffers: k[0..5], stage, f_fast, f_implicit
-  while ((int)c->rs_bufs.size() < s + 3) {
+  // buffers: k[0..s-1], stage, f_fast, f_implicit, entry backup
+  while ((int)c->rs_bufs.size() < s + 4) {
     double* p = nullptr;
     MR_CUDA_TRY(c, cudaMalloc(&p, c->dof * sizeof(double)));
     c->rs_bufs.push_back(p);
@@ -2001,9 +1996,12 @@ int mr_reference_solution(mr_ctx* c, double t0, double tf, double h, int* fail_s
   double* stage = c->rs_bufs[s];
   double* tf_ = c->rs_bufs[s + 1];
   double* ti_ = c->rs_bufs[s + 2];
+  double* backup = c->rs_bufs[s + 3];
   const bool fast = c->fast_kind != FK_NONE, slow = c->slow_kind != SK_NONE;
   const bool imp = c->slow_kind == SK_STENCIL && c->imex;
   cudaStream_t st = c->stream;
+  MR_CUDA_TRY(c, cudaMemcpyAsync(backup, c->y_state, c->dof * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, st));
   const long n_steps = (long)std::ceil((tf - t0) / h - 1e-12);
   double t = t0;
   for (long n = 0; n < n_steps; ++n) {
@@ -2014,9 +2012,9 @@ int mr_reference_solution(mr_ctx* c, double t0, double tf, double h, int* fail_s
       double cf[MR_MAXREF];
       int nref = 0;
       for (int j = 0; j < i; ++j)
-        if (A[i][j] != 0.0) {
+        if (A[i * s + j] != 0.0) {
           f[nref] = k[j];
-          cf[nref++] = step * A[i][j];
+          cf[nref++] = step * A[i * s + j];
         }
       MR_CUDA_TRY(c, launch_update(c->y_state, stage, nref, f, cf, c->dof, i, c->d_fail, st));
       c->launches++;
@@ -2062,13 +2060,41 @@ int mr_reference_solution(mr_ctx* c, double t0, double tf, double h, int* fail_s
     if (*c->h_fail != MR_NO_FAIL) {
       const int fs = (int)(*c->h_fail >> 40);
       if (fail_stage) *fail_stage = fs;
+      if (evals) *evals += (uint64_t)(fs < s ? fs : s);  // stages evaluated before the throw
+      MR_CUDA_TRY(c, cudaMemcpyAsync(c->y_state, backup, c->dof * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, st));
+      MR_CUDA_TRY(c, cudaStreamSynchronize(st));
       return set_err(c, MR_INTEGRATION,
                      fs == s ? "erk_step: non-finite result" : "erk_step: non-finite stage value");
     }
+    if (evals) *evals += (uint64_t)s;
     std::swap(c->y_state, c->y_work);
     t = (n == n_steps - 1) ? tf : t0 + (double)(n + 1) * h;
   }
   return MR_OK;
+}
+
+int mr_erk_integrate(mr_ctx* c, int s, const double* A, const double* b, const double* cvec,
+                     double t0, double tf, double h, uint64_t* n_explicit_evals, int* fail_stage)
+{
+  (void)cvec;  // sum_rhs of the plugins is autonomous: t + c_i h is not consumed
+  if (!c || !A || !b) return MR_CONTRACT;
+  return erk_integrate_dev(c, s, A, b, t0, tf, h, n_explicit_evals, fail_stage);
+}
+
+// reference_solution (erk.cpp:59-75): erk_integrate of cash-karp5
+// (butcher.cpp:305-321, written exactly as there), no counters.
+int mr_reference_solution(mr_ctx* c, double t0, double tf, double h, int* fail_stage)
+{
+  double A[6][6] = {{0}}, b[6] = {0};
+  A[1][0] = 1.0 / 5.0;
+  A[2][0] = 3.0 / 40.0; A[2][1] = 9.0 / 40.0;
+  A[3][0] = 3.0 / 10.0; A[3][1] = -9.0 / 10.0; A[3][2] = 6.0 / 5.0;
+  A[4][0] = -11.0 / 54.0; A[4][1] = 5.0 / 2.0; A[4][2] = -70.0 / 27.0; A[4][3] = 35.0 / 27.0;
+  A[5][0] = 1631.0 / 55296.0; A[5][1] = 175.0 / 512.0; A[5][2] = 575.0 / 13824.0;
+  A[5][3] = 44275.0 / 110592.0; A[5][4] = 253.0 / 4096.0;
+  b[0] = 37.0 / 378.0; b[2] = 250.0 / 621.0; b[3] = 125.0 / 594.0; b[5] = 512.0 / 1771.0;
+  return erk_integrate_dev(c, 6, &A[0][0], b, t0, tf, h, nullptr, fail_stage);
 }
 
 int mr_slow_rhs(mr_ctx* c, double t, const double* y, double* out)

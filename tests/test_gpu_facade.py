@@ -75,10 +75,10 @@ def test_facade_imex_modes_agree():
 
 
 @pytest.mark.skipif(not os.path.exists(LIB), reason="facade test library not built (needs the reference)")
-@pytest.mark.parametrize("which", [0, 1])
+@pytest.mark.parametrize("which", [0, 1, 2])
 def test_facade_refsol_and_ark(which):
-    """b200::reference_solution / b200::ark_imex_integrate vs the reference's
-    reference_solution / ark_imex_integrate on the CPU physics."""
+    """b200::reference_solution / ark_imex_integrate / erk_integrate vs the
+    reference's own functions on the CPU physics (erk: equal evaluation count)."""
     L = C.CDLL(LIB)
     cfg = dict(CONFIGS["C5"])
     S, R, n = cfg["S"], cfg["R"], 8
@@ -91,15 +91,17 @@ def test_facade_refsol_and_ark(which):
     cnt = np.zeros(16, dtype=np.uint64)
     err = C.create_string_buffer(512)
     dp = C.POINTER(C.c_double)
-    h, steps = (2e-17, 4) if which == 0 else (2e-3, 2)
+    h, steps = (2e-3, 2) if which == 1 else (2e-17, 4)
     rc = L.facade_selftest2(
         C.c_int(which), C.c_int(n), C.c_int(S), C.c_int(R), C.c_double(cfg["rho"]),
         sp.ctypes.data_as(dp), rx.ctypes.data_as(dp), rs.ctypes.data_as(C.POINTER(C.c_int)),
         y0.ctypes.data_as(dp), C.c_int(8), C.c_double(0.0), C.c_double(0.05), C.c_int(8),
-        C.c_int(1 if which == 0 else 0), C.c_double(h), C.c_int(steps),
+        C.c_int(0 if which == 1 else 1), C.c_double(h), C.c_int(steps),
         newton.ctypes.data_as(dp), weights.ctypes.data_as(dp), errs.ctypes.data_as(dp),
         cnt.ctypes.data_as(C.POINTER(C.c_uint64)), err, C.c_size_t(512))
     assert rc == 0, err.value.decode()
     assert errs[0] <= 1e-10 * steps, errs
     if which == 1:
         assert solver_counts_ok(cnt[0:8], cnt[8:16], 8)
+    if which == 2:
+        assert cnt[2] == cnt[10] == steps * 3

@@ -138,3 +138,37 @@ def test_reference_solution_fixture_bitwise(key):
     h = meta["h_ref"]
     y = sysm.reference_solution(0.0, meta["steps"] * h, h, y0)
     assert np.array_equal(y, FIX[key + "_y"])
+
+
+@pytest.mark.skipif(not os.path.isdir(O.REF_SRC) and not os.path.exists(O.REF_LIB),
+                    reason="reference build unavailable")
+@pytest.mark.parametrize("table", ["classic-rk4", "kutta3", "cash-karp5"])
+def test_erk_integrate_equals_reference_live(table):
+    """erk_integrate (erk.cpp:40-57) on sum_rhs -- the harness's erk-<table>
+    family -- restated bit-for-bit, with the reference's evaluation count."""
+    cfg, sysm = physics("C1", 6)
+    y0 = sysm.initial_condition(7)
+    h = cfg["H"] / 20
+    a, ea = sysm.erk_integrate(table, 0.0, 2.5 * h, h, y0)
+    b, eb = sysm.erk_integrate(table, 0.0, 2.5 * h, h, y0, use_reference=True)
+    stages = {"classic-rk4": 4, "kutta3": 3, "cash-karp5": 6}[table]
+    assert np.array_equal(a, b)
+    assert ea == eb == 3 * stages  # ceil(2.5) steps
+    if table == "cash-karp5":
+        assert np.array_equal(a, sysm.reference_solution(0.0, 2.5 * h, h, y0))
+
+
+def test_erk_integrate_failure_counts():
+    """erk_step's throw (erk.cpp:24-26): stage index and the evaluations made
+    before it, restated."""
+    big = np.array([[1e200, 0.0], [0.0, 1e200]])
+    lin = O.System(1, 1, 1, 2, fast="linear", slow="linear", fast_A=big, slow_A=np.zeros((2, 2)))
+    y0 = np.array([1e200, 1e200])
+    with pytest.raises(O.StepError) as e:
+        lin.erk_integrate("classic-rk4", 0.0, 1.0, 0.5, y0)
+    assert e.value.stage >= 0 and int(e.value.counters[0]) == e.value.stage
+    if O.ref_available():
+        with pytest.raises(O.StepError) as r:
+            lin.erk_integrate("classic-rk4", 0.0, 1.0, 0.5, y0, use_reference=True)
+        assert r.value.stage == e.value.stage
+        assert int(r.value.counters[0]) == int(e.value.counters[0])
