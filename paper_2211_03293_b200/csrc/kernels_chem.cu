@@ -58,7 +58,8 @@ int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int nd
 // fit the 227 KB shared memory of an SM (one block for NW = 16)
 int chem_chunking(int NW, int S, int R, size_t blob_bytes, int* rc, int* nchunk)
 {
-  const size_t budget = (size_t)(NW <= 8 ? 113 : 227) * 1024;  // 2 blocks/SM for NW <= 8
+  size_t budget = (size_t)(NW <= 8 ? 113 : 227) * 1024;  // 2 blocks/SM for NW <= 8
+  if (const char* env = getenv("MR_CHEM_BUDGET_KB")) budget = (size_t)atoi(env) * 1024;  // experiment hook
   const size_t fixed = mrchem::smem_bytes(NW, S + 1, 0, (int)((blob_bytes + 15) / 16));
   if (fixed >= budget) return 1;
   int cap = (int)((budget - fixed) / 256);
