@@ -250,6 +250,36 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// mbarrier helpers (CTA scope): per-slot full/empty barriers of a cp.async ring
+__device__ __forceinline__ unsigned smem_u32(const void* p)
+{
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count)
+{
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b)
+{
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(b))
+               : "memory");
+}
+// arrive once this thread's prior cp.async copies have landed (count preset)
+__device__ __forceinline__ void mbar_cp_async_arrive(unsigned long long* b)
+{
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity)
+{
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "MR_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra MR_WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
 #ifndef MR_V2_TJ
 #define MR_V2_TJ 8
 #endif
@@ -423,20 +453,38 @@ __global__ void __launch_bounds__(kV2Threads, (kV2Threads <= 256 ? 2 : 1)) stenc
 #ifndef MR_V3_TJ
 #define MR_V3_TJ 16
 #endif
-constexpr int kV3TJ = MR_V3_TJ, kV3PF = 4;  // measured: PF 2/3/4/6 -> 45/46/51/40% of HBM at 256^3
-constexpr int kV3Threads = 16 * kV3TJ;      // 2 x 2 points per thread
+#ifndef MR_V3_PF
+#define MR_V3_PF 4
+#endif
+constexpr int kV3TJ = MR_V3_TJ, kV3PF = MR_V3_PF;  // block-barrier version measured: PF 2/3/4/6 -> 45/46/51/40% of HBM at 256^3
+constexpr int kV3Threads = 16 * kV3TJ;      // 2 x 2 points per thread (compute threads)
+#ifndef MR_V3_PRODUCER
+#define MR_V3_PRODUCER 0
+#endif
+// + one producer warp that fills the ring (MR_V3_PRODUCER, needs MR_V3_MBAR)
+constexpr int kV3Block = kV3Threads + (MR_V3_PRODUCER ? 32 : 0);
+#ifndef MR_V3_MBAR
+#define MR_V3_MBAR 1
+#endif
+#ifndef MR_V3_LATE_ISSUE
+#define MR_V3_LATE_ISSUE 1
+#endif
 template <int M>
 constexpr size_t v3_smem_bytes()
 {
-  return (size_t)(M + kV3PF + 1) * (kV3TJ + 2 * M) * (kV2TK + 2 * M) * sizeof(double);
+  // ring [R][RJ][RK] + (MR_V3_MBAR) full[R] and empty[R] mbarriers
+  return (size_t)(M + kV3PF + 1) * (kV3TJ + 2 * M) * (kV2TK + 2 * M) * sizeof(double) +
+         (MR_V3_MBAR ? 2 * (M + kV3PF + 1) * sizeof(unsigned long long) : 0);
 }
 
 // K2 v3 (order 8): as v2 with a 2 x 2 register block per thread (rows jl,
 // jl+1) -- the axis-1 rows jl - m and jl + 1 + m each serve two outputs per
 // column pair, cutting the shared wavefronts per point by ~30% -- one
-// 256-thread block per SM (251 registers) and a 4-plane prefetch.
+// 256-thread block per SM (240 registers) and a 4-plane prefetch.  The plane
+// ring is synchronised by per-slot full/empty mbarriers (MR_V3_MBAR): no block
+// barrier in the march, so warps drift up to two planes apart.
 template <int M>
-__global__ void __launch_bounds__(kV3Threads, 256 / kV3Threads) stencil_v3_kernel(const StencilArgs a, int iper)
+__global__ void __launch_bounds__(kV3Block, 1) stencil_v3_kernel(const StencilArgs a, int iper)
 {
   constexpr int PF = kV3PF;
   constexpr int RJ = kV3TJ + 2 * M, RK = kV2TK + 2 * M, R = M + PF + 1;
@@ -478,8 +526,60 @@ __global__ void __launch_bounds__(kV3Threads, 256 / kV3Threads) stencil_v3_kerne
       coff_dst[u] = r * RK + CW * cc;
     }
   }
+#if MR_V3_MBAR
+  // full[s]: the kThreads cp.async arrivals of the plane in slot s; empty[s]:
+  // one arrival per warp when it has finished reading the plane in slot s.
+  // Warps run up to one plane apart instead of meeting at a block barrier.
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)R * RJ * RK);
+  unsigned long long* empty = full + R;
+  if (tid == 0) {
+    for (int q = 0; q < R; ++q) {
+      mbar_init(full + q, MR_V3_PRODUCER ? 32 : kThreads);
+      mbar_init(empty + q, kThreads / 32);
+    }
+  }
+  __syncthreads();
+#endif
+#if MR_V3_PRODUCER
+  static_assert(MR_V3_MBAR, "the producer warp needs the mbarrier ring");
+  if (ty == kV3TJ / 2) {  // producer warp: planes ib - ... ie + M - 1 into the ring
+    constexpr int NP = (RJ * CPR + 31) / 32;
+    int ps[NP], pd[NP];
+#pragma unroll
+    for (int u = 0; u < NP; ++u) {
+      const int c = tx + 32 * u;
+      pd[u] = -1;
+      ps[u] = 0;
+      if (c < RJ * CPR) {
+        const int r = c / CPR, cc = c - r * CPR;
+        ps[u] = ((j0 - M + r + n1) % n1) * n2 + (k0 - M + CW * cc + n2) % n2;
+        pd[u] = r * RK + CW * cc;
+      }
+    }
+    const int nfill = ie + M - ib;
+    for (int rel = 0; rel < nfill; ++rel) {
+      const int sl = rel % R;
+      if (rel >= R) mbar_wait(empty + sl, (unsigned)((rel - R) / R) & 1u);
+      const double* src = plane_ptr(ib + rel);
+      double* dst = ring + (size_t)sl * RJ * RK;
+#pragma unroll
+      for (int u = 0; u < NP; ++u) {
+        if (pd[u] < 0) continue;
+        if constexpr (CW == 2) cp_async16(dst + pd[u], src + ps[u]);
+        else cp_async8(dst + pd[u], src + ps[u]);
+      }
+      mbar_cp_async_arrive(full + sl);
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    return;
+  }
+#endif
   auto issue_to = [&](int ip, double* dst) {
-    if (ip < ie + M) {
+    if (!MR_V3_PRODUCER && ip < ie + M) {
+#if MR_V3_MBAR
+      const int rel = ip - ib, sl = rel % R;
+      if (rel >= R) mbar_wait(empty + sl, (unsigned)((rel - R) / R) & 1u);  // previous occupant read
+#endif
       const double* src = plane_ptr(ip);
 #pragma unroll
       for (int u = 0; u < NCH; ++u) {
@@ -487,10 +587,24 @@ __global__ void __launch_bounds__(kV3Threads, 256 / kV3Threads) stencil_v3_kerne
         if constexpr (CW == 2) cp_async16(dst + coff_dst[u], src + coff_src[u]);
         else cp_async8(dst + coff_dst[u], src + coff_src[u]);
       }
+#if MR_V3_MBAR
+      mbar_cp_async_arrive(full + sl);
+#endif
     }
+#if !MR_V3_MBAR
     cp_async_commit();
+#endif
   };
   auto issue = [&](int ip) { issue_to(ip, slot(ip)); };
+  // this thread may read plane ip from the ring (its copies landed, all threads')
+  auto ready = [&](int ip) {
+#if MR_V3_MBAR
+    const int rel = ip - ib;
+    mbar_wait(full + rel % R, (unsigned)(rel / R) & 1u);
+#else
+    (void)ip;
+#endif
+  };
   auto pair = [&](const double* t, int r, int c, double& v0, double& v1) {
     if constexpr (M % 2 == 0) {
       const double2 v = *reinterpret_cast<const double2*>(t + r * RK + c);
@@ -528,8 +642,13 @@ __global__ void __launch_bounds__(kV3Threads, 256 / kV3Threads) stencil_v3_kerne
       qv[2 * e][q] = __ldg(src);
       qv[2 * e + 1][q] = __ldg(src + 1);
     }
+#if MR_V3_MBAR
+#pragma unroll
+  for (int q = M; q < 2 * M; ++q) ready(ib - M + q);
+#else
   cp_async_wait<PF>();
   __syncthreads();
+#endif
 #pragma unroll
   for (int q = M; q < 2 * M; ++q)
 #pragma unroll
@@ -542,8 +661,10 @@ __global__ void __launch_bounds__(kV3Threads, 256 / kV3Threads) stencil_v3_kerne
       const int t = t0 + ph;
       if (t >= nplanes) break;
       const int i = ib + t;
+#if !MR_V3_MBAR
       cp_async_wait<PF - 1>();
       __syncthreads();
+#endif
       // ring slots: compile-time when the ring and the register queue have the
       // same period (R == Q, t0 a multiple of Q)
 #ifndef MR_V3_CSLOT
@@ -553,7 +674,10 @@ __global__ void __launch_bounds__(kV3Threads, 256 / kV3Threads) stencil_v3_kerne
       double* const s_iss = kCs ? ring + (size_t)((ph + M + PF) % R) * RJ * RK : slot(i + M + PF);
       const double* const tq = kCs ? ring + (size_t)((ph + M) % R) * RJ * RK : slot(i + M);
       const double* const tc = kCs ? ring + (size_t)(ph % R) * RJ * RK : slot(i);
+#if !MR_V3_MBAR || !MR_V3_LATE_ISSUE
       issue_to(i + M + PF, s_iss);
+#endif
+      ready(i + M);
 #pragma unroll
       for (int e = 0; e < 2; ++e) pair(tq, jl + e, kl, qv[2 * e][(ph + 2 * M) % Q], qv[2 * e + 1][(ph + 2 * M) % Q]);
       const int ig = a.i0 + i;
@@ -632,9 +756,18 @@ __global__ void __launch_bounds__(kV3Threads, 256 / kV3Threads) stencil_v3_kerne
             make_double2(acc[2 * e], acc[2 * e + 1]);
 #endif
       }
+#if MR_V3_MBAR
+      __syncwarp();
+      if (tx == 0) mbar_arrive(empty + (unsigned)t % R);  // this warp is done with plane i
+#if MR_V3_LATE_ISSUE
+      issue_to(i + M + PF, s_iss);  // waits for the other warps to finish plane i - 1
+#endif
+#endif
     }
   }
+#if !MR_V3_MBAR
   cp_async_wait<0>();
+#endif
 }
 
 // halo planes: send_lo = first g planes, send_hi = last g planes, per component
@@ -798,7 +931,7 @@ cudaError_t launch_stencil(const StencilArgs& a, cudaStream_t st)
     while (iper > 16 && tiles * ((a.n0l + iper - 1) / iper) < 148 * 8) iper = (iper + 1) / 2;
     const unsigned nch = (unsigned)((a.n0l + iper - 1) / iper);
     dim3 grid(a.n2 / kV2TK, a.n1 / kV3TJ, (unsigned)a.ncomp * nch);
-    dim3 block(32, kV3TJ / 2);
+    dim3 block(32, kV3Block / 32);
     if (a.M == 1) {
       cudaFuncSetAttribute(stencil_v3_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3_smem_bytes<1>());
       stencil_v3_kernel<1><<<grid, block, v3_smem_bytes<1>(), st>>>(a, iper);
