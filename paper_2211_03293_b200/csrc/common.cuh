@@ -98,7 +98,8 @@ struct ChemParams {
 };
 
 struct ChemCfg {
-  int NW, SPL;  // warps per block (slots), components per thread
+  int NW, SPL;  // warps per cell group (slots), components per thread
+  int NG;       // cell groups (of 32 cells) per block, named barriers per group
   bool subdiag;
   int ndeg;
 };
@@ -163,7 +164,7 @@ cudaError_t launch_fast_rhs(const ChainCfg& cfg, const double* y, double* out, s
 size_t chain_smem_bytes(const ChainCfg& cfg, int S, int R, int block);
 
 int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int ndeg);
-int chem_chunking(int NW, int S, int R, size_t blob_bytes, int* rc, int* nchunk);
+int chem_chunking(int NW, int S, int R, size_t blob_bytes, int* rc, int* nchunk, int NG = 1);
 cudaError_t launch_chem_chain(const ChemCfg& cfg, const ChainArgs& a, const ChemParams& P,
                               cudaStream_t st);
 cudaError_t launch_chem_rhs(const ChemCfg& cfg, const double* y, double* out, size_t ncell,

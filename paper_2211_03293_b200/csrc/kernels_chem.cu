@@ -22,6 +22,13 @@ MR_DECL(16, 4)
 MR_DECL(24, 3)
 MR_DECL(32, 2)
 #undef MR_DECL
+#define MR_DECL_G(A, B, G)                                                                      \
+  extern template cudaError_t run_chem_chain<A, B, true, 4, 1, G>(const ChainArgs&, const ChemParams&, cudaStream_t);  \
+  extern template cudaError_t run_chem_chain<A, B, true, 4, 2, G>(const ChainArgs&, const ChemParams&, cudaStream_t);  \
+  extern template cudaError_t run_chem_chain<A, B, false, 6, 1, G>(const ChainArgs&, const ChemParams&, cudaStream_t); \
+  extern template cudaError_t run_chem_chain<A, B, false, 6, 2, G>(const ChainArgs&, const ChemParams&, cudaStream_t);
+MR_DECL_G(16, 4, 2)
+#undef MR_DECL_G
 }  // namespace mrchem
 
 // (NW warps = slots, SPL components per thread) layouts
@@ -37,10 +44,14 @@ int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int nd
       if (tab.A[i][j] != 0.0) subdiag = false;
   cfg->subdiag = subdiag;
   cfg->ndeg = ndeg;
+  cfg->NG = 1;
   if (ncomp <= 12) { cfg->NW = 4; cfg->SPL = 3; }
   else if (ncomp <= 24) { cfg->NW = 8; cfg->SPL = 3; }
   else if (ncomp <= 64) { cfg->NW = 32; cfg->SPL = 2; }
   else return 1;
+  if (const char* env = getenv("MR_CHEM_NG")) {  // experiment hook: two 32-cell groups per block
+    if (atoi(env) == 2 && ncomp <= 64 && ncomp >= 33) { cfg->NW = 16; cfg->SPL = 4; cfg->NG = 2; return 0; }
+  }
   if (const char* env = getenv("MR_CHEM_BLOCK")) {  // experiment hook "NW,SPL"
     int nw = 0, spl = 0;
     if (sscanf(env, "%d,%d", &nw, &spl) == 2 && nw * spl >= ncomp) {
@@ -56,13 +67,14 @@ int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int nd
 
 // rate-buffer chunking: largest chunk (multiple of NW) such that two blocks
 // fit the 227 KB shared memory of an SM (one block for NW = 16)
-int chem_chunking(int NW, int S, int R, size_t blob_bytes, int* rc, int* nchunk)
+int chem_chunking(int NW, int S, int R, size_t blob_bytes, int* rc, int* nchunk, int NG)
 {
   size_t budget = (size_t)(NW <= 8 ? 113 : 227) * 1024;  // 2 blocks/SM for NW <= 8
+  if (NG > 1) budget = 227 * 1024;
   if (const char* env = getenv("MR_CHEM_BUDGET_KB")) budget = (size_t)atoi(env) * 1024;  // experiment hook
-  const size_t fixed = mrchem::smem_bytes(NW, S + 1, 0, (int)((blob_bytes + 15) / 16));
+  const size_t fixed = mrchem::smem_bytes(NW, S + 1, 0, (int)((blob_bytes + 15) / 16), NG);
   if (fixed >= budget) return 1;
-  int cap = (int)((budget - fixed) / 256);
+  int cap = (int)((budget - fixed) / (256 * (size_t)NG));
   cap -= cap % NW;
   if (cap < NW) return 1;
   int n = (R + cap - 1) / cap;
@@ -78,7 +90,7 @@ cudaError_t launch_chem_chain(const ChemCfg& cfg, const ChainArgs& a, const Chem
                               cudaStream_t st)
 {
 #define MR_CHEM_DISPATCH(A, B)                                                              \
-  if (cfg.NW == A && cfg.SPL == B) {                                                        \
+  if (cfg.NW == A && cfg.SPL == B && cfg.NG == 1) {                                         \
     if (cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem_chain<A, B, true, 4, 1>(a, P, st);   \
     if (cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem_chain<A, B, true, 4, 2>(a, P, st);   \
     if (!cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem_chain<A, B, false, 6, 1>(a, P, st); \
@@ -86,6 +98,12 @@ cudaError_t launch_chem_chain(const ChemCfg& cfg, const ChainArgs& a, const Chem
   }
   MR_CHEM_BLOCK_LAYOUTS(MR_CHEM_DISPATCH)
 #undef MR_CHEM_DISPATCH
+  if (cfg.NW == 16 && cfg.SPL == 4 && cfg.NG == 2) {
+    if (cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem_chain<16, 4, true, 4, 1, 2>(a, P, st);
+    if (cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem_chain<16, 4, true, 4, 2, 2>(a, P, st);
+    if (!cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem_chain<16, 4, false, 6, 1, 2>(a, P, st);
+    if (!cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem_chain<16, 4, false, 6, 2, 2>(a, P, st);
+  }
   return cudaErrorInvalidConfiguration;
 }
 

@@ -1362,7 +1362,7 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
                               4 * ((size_t)nnz + 2 * 3 * (size_t)S * MR_CHEM_MAXCHUNK) + 16;
     int rcz = 0, nch = 0;
     if (chem_pick(&lay, S + 1, S, R, t4, 1) ||
-        chem_chunking(lay.NW, S, R, blob_bound, &rcz, &nch))
+        chem_chunking(lay.NW, S, R, blob_bound, &rcz, &nch, lay.NG))
       return set_err(c, MR_CONTRACT, "mechanism too large for the chemistry kernel's shared memory");
     P.rc = rcz;
     P.nchunk = nch;
