@@ -342,6 +342,8 @@ def run_ours(args):
                              "algorithmic_bytes_per_launch"),
                          "traffic_source": tr.get("chem_chain", {}).get("source"),
                          "flops_per_eval": flops_per_eval,
+                         "ncu_fp64_pipe_pct": tr.get("chem_chain", {}).get("fp64_pipe_pct"),
+                         "ncu_lsu_wavefronts_pct": tr.get("chem_chain", {}).get("lsu_wavefronts_pct"),
                          "peak_source": "DFMA-chain microbenchmark in this run (MEASURED_PEAKS.json "
                                         "has no fp64 figure)"},
             "roofline_stencil": {"bound": "hbm", "achieved": stencil_gbs,
@@ -351,7 +353,8 @@ def run_ours(args):
                                  "traffic_algorithmic": tr.get("stencil", {}).get(
                                      "algorithmic_bytes_per_launch"),
                                  "traffic_source": tr.get("stencil", {}).get("source"),
-                                 "bytes_per_eval": 16.0 * (S + 1) * ncell_local},
+                                 "bytes_per_eval": 16.0 * (S + 1) * ncell_local,
+                                 "ncu_fp64_pipe_pct": tr.get("stencil", {}).get("fp64_pipe_pct")},
             "time_split_ms": {"chem": chem_ms_max, "slow": slow_ms_max, "other": other_ms,
                               "profiled_total": profiled_ms, "steps": args.steps},
             "e2e": e2e,

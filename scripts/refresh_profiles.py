@@ -59,5 +59,10 @@ for key, name, alg, note in [
                "algorithmic_bytes_per_launch": alg,
                "duration_ms": float(dur) / (1e3 if unit == "us" else 1.0),
                "source": f"{dst}/{name}.ncu-rep", "note": note}
+    for k, metric in [("fp64_pipe_pct", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                      ("lsu_wavefronts_pct", "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+                      ("issue_active_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active")]:
+        if metric in d:
+            tr[key][k] = float(d[metric][0])
 json.dump(tr, open(f"{dst}/traffic.json", "w"), indent=1)
 print("profiles refreshed from", tag)
