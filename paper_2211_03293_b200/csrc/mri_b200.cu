@@ -1443,7 +1443,10 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
   double f = 0.0;
   f += 8.0 + cl + 3.0;                      // T(e) root, log T, 1/T, RT/P, P/RT
   f += S * (6.0 + 6.0 + ce + 5.0 + 1.0);    // e(T) sums, g, exp, C/E'/D', W/rho
-  f += R * (4.0 + ce + 6.0);                // kf exponent, exp, forward/reverse, q
+  for (int j = 0; j < R; ++j) {              // kf exponent, exp, forward/reverse, q:
+    const int nr = 1 + (rspecies[4 * j + 1] >= 0), np = 1 + (rspecies[4 * j + 3] >= 0);
+    f += 4.0 + ce + 2.0 + 2.0 * (nr - 1) + (np - 1);  // products of present operands only
+  }
   f += cnt[S];                              // production sums
   f += (S + 1) * 7.0;                       // forcing Horner + f + r, stage, out
   c->chem_flops = f;
