@@ -469,11 +469,13 @@ constexpr int kV3Block = kV3Threads + (MR_V3_PRODUCER ? 32 : 0);
 #ifndef MR_V3_LATE_ISSUE
 #define MR_V3_LATE_ISSUE 1
 #endif
+constexpr int kV3MaxPlanes = 512;  // planes per block (iper) staged profile terms
 template <int M>
 constexpr size_t v3_smem_bytes()
 {
   // ring [R][RJ][RK] + (MR_V3_MBAR) full[R] and empty[R] mbarriers
   return (size_t)(M + kV3PF + 1) * (kV3TJ + 2 * M) * (kV2TK + 2 * M) * sizeof(double) +
+         2 * kV3MaxPlanes * sizeof(double) +  // per-plane velocity-profile terms
          (MR_V3_MBAR ? 2 * (M + kV3PF + 1) * sizeof(unsigned long long) : 0);
 }
 
@@ -483,7 +485,7 @@ constexpr size_t v3_smem_bytes()
 // 256-thread block per SM (240 registers) and a 4-plane prefetch.  The plane
 // ring is synchronised by per-slot full/empty mbarriers (MR_V3_MBAR): no block
 // barrier in the march, so warps drift up to two planes apart.
-template <int M>
+template <int M, int VK>
 __global__ void __launch_bounds__(kV3Block, 1) stencil_v3_kernel(const StencilArgs a, int iper)
 {
   constexpr int PF = kV3PF;
@@ -522,10 +524,21 @@ __global__ void __launch_bounds__(kV3Block, 1) stencil_v3_kernel(const StencilAr
       const int r = c / CPR, cc = c - r * CPR;
       const int jr = (j0 - M + r + n1) % n1;
       const int kr = (k0 - M + CW * cc + n2) % n2;
-      coff_src[u] = jr * n2 + kr;
+      coff_src[u] = (jr * n2 + kr) * (int)sizeof(double);  // bytes
       coff_dst[u] = r * RK + CW * cc;
     }
   }
+  // plane-dependent profile terms of u_1 and u_2 for this block's planes
+  // (after the ring and its mbarriers)
+  double* sprof = reinterpret_cast<double*>(ring + (size_t)R * RJ * RK + (MR_V3_MBAR ? 2 * R : 0));
+  if constexpr (VK == 1)
+    for (int q = tid; q < ie - ib; q += kThreads) {
+      sprof[q] = a.prof[(1 * 2 + 0) * a.nmax + a.i0 + ib + q];
+      sprof[kV3MaxPlanes + q] = a.prof[(2 * 2 + 0) * a.nmax + a.i0 + ib + q];
+    }
+#if !MR_V3_MBAR
+  __syncthreads();
+#endif
 #if MR_V3_MBAR
   // full[s]: the kThreads cp.async arrivals of the plane in slot s; empty[s]:
   // one arrival per warp when it has finished reading the plane in slot s.
@@ -580,7 +593,7 @@ __global__ void __launch_bounds__(kV3Block, 1) stencil_v3_kernel(const StencilAr
       const int rel = ip - ib, sl = rel % R;
       if (rel >= R) mbar_wait(empty + sl, (unsigned)((rel - R) / R) & 1u);  // previous occupant read
 #endif
-      const double* src = plane_ptr(ip);
+      const char* src = reinterpret_cast<const char*>(plane_ptr(ip));
 #pragma unroll
       for (int u = 0; u < NCH; ++u) {
         if (coff_dst[u] < 0) continue;
@@ -627,9 +640,22 @@ __global__ void __launch_bounds__(kV3Block, 1) stencil_v3_kernel(const StencilAr
   double cadv0[4];  // u_0 depends on (j, k): constant along the march
 #pragma unroll
   for (int p = 0; p < 4; ++p)
-    cadv0[p] = (a.vel_kind == 0 ? a.u[0]
-                                : P[(0 * 2 + 0) * nm + jA + (p >> 1)] + P[(0 * 2 + 1) * nm + kA + (p & 1)]) *
+    cadv0[p] = (VK == 0 ? a.u[0]
+                        : P[(0 * 2 + 0) * nm + jA + (p >> 1)] + P[(0 * 2 + 1) * nm + kA + (p & 1)]) *
                a.inv_dx[0];
+#ifndef MR_V3_HOIST
+#define MR_V3_HOIST 1  // measured: 56.5 -> 58.4% of HBM at 256^3
+#endif
+#if MR_V3_HOIST
+  double pk1[2], pj2[2];  // per-thread profile terms of u_1 (k) and u_2 (j)
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    pk1[e] = VK == 0 ? 0.0 : P[(1 * 2 + 1) * nm + kA + e];
+    pj2[e] = VK == 0 ? 0.0 : P[(2 * 2 + 1) * nm + jA + e];
+  }
+#endif
+  // output rows jA, jA + 1 of plane i: running pointer
+  double* orow = a.out + (size_t)comp * ncell + (size_t)ib * plane + (size_t)jA * n2 + kA;
 
   constexpr int Q = 2 * M + 1;
   for (int q = 0; q < M + PF; ++q) issue(ib + q);
@@ -684,10 +710,15 @@ __global__ void __launch_bounds__(kV3Block, 1) stencil_v3_kernel(const StencilAr
       double cadv1[2], cadv2[2];  // u_1 depends on (i, k), u_2 on (i, j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        cadv1[e] = (a.vel_kind == 0 ? a.u[1] : P[(1 * 2 + 0) * nm + ig] + P[(1 * 2 + 1) * nm + kA + e]) *
+#if MR_V3_HOIST
+        cadv1[e] = (VK == 0 ? a.u[1] : sprof[t] + pk1[e]) * a.inv_dx[1];
+        cadv2[e] = (VK == 0 ? a.u[2] : sprof[kV3MaxPlanes + t] + pj2[e]) * a.inv_dx[2];
+#else
+        cadv1[e] = (VK == 0 ? a.u[1] : P[(1 * 2 + 0) * nm + ig] + P[(1 * 2 + 1) * nm + kA + e]) *
                    a.inv_dx[1];
-        cadv2[e] = (a.vel_kind == 0 ? a.u[2] : P[(2 * 2 + 0) * nm + ig] + P[(2 * 2 + 1) * nm + jA + e]) *
+        cadv2[e] = (VK == 0 ? a.u[2] : P[(2 * 2 + 0) * nm + ig] + P[(2 * 2 + 1) * nm + jA + e]) *
                    a.inv_dx[2];
+#endif
       }
       const int cq = (ph + M) % Q;
       double acc[4];
@@ -748,7 +779,7 @@ __global__ void __launch_bounds__(kV3Block, 1) stencil_v3_kernel(const StencilAr
       }
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        double* o = a.out + (size_t)comp * ncell + (size_t)i * plane + (size_t)(jA + e) * n2 + kA;
+        double* o = orow + (size_t)e * n2;
         *reinterpret_cast<double2*>(o) =
 #if MR_V3_SPLIT
             make_double2(acc[2 * e] + acc1[2 * e], acc[2 * e + 1] + acc1[2 * e + 1]);
@@ -756,6 +787,7 @@ __global__ void __launch_bounds__(kV3Block, 1) stencil_v3_kernel(const StencilAr
             make_double2(acc[2 * e], acc[2 * e + 1]);
 #endif
       }
+      orow += plane;
 #if MR_V3_MBAR
       __syncwarp();
       if (tx == 0) mbar_arrive(empty + (unsigned)t % R);  // this warp is done with plane i
@@ -929,18 +961,34 @@ cudaError_t launch_stencil(const StencilArgs& a, cudaStream_t st)
     const size_t tiles = (size_t)(a.n1 / kV3TJ) * (a.n2 / kV2TK) * a.ncomp;
     int iper = a.n0l;
     while (iper > 16 && tiles * ((a.n0l + iper - 1) / iper) < 148 * 8) iper = (iper + 1) / 2;
+    while (iper > kV3MaxPlanes) iper = (iper + 1) / 2;
     const unsigned nch = (unsigned)((a.n0l + iper - 1) / iper);
     dim3 grid(a.n2 / kV2TK, a.n1 / kV3TJ, (unsigned)a.ncomp * nch);
     dim3 block(32, kV3Block / 32);
     if (a.M == 1) {
-      cudaFuncSetAttribute(stencil_v3_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3_smem_bytes<1>());
-      stencil_v3_kernel<1><<<grid, block, v3_smem_bytes<1>(), st>>>(a, iper);
+      if (a.vel_kind == 0) {
+        cudaFuncSetAttribute(stencil_v3_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3_smem_bytes<1>());
+        stencil_v3_kernel<1, 0><<<grid, block, v3_smem_bytes<1>(), st>>>(a, iper);
+      } else {
+        cudaFuncSetAttribute(stencil_v3_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3_smem_bytes<1>());
+        stencil_v3_kernel<1, 1><<<grid, block, v3_smem_bytes<1>(), st>>>(a, iper);
+      }
     } else if (a.M == 2) {
-      cudaFuncSetAttribute(stencil_v3_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3_smem_bytes<2>());
-      stencil_v3_kernel<2><<<grid, block, v3_smem_bytes<2>(), st>>>(a, iper);
+      if (a.vel_kind == 0) {
+        cudaFuncSetAttribute(stencil_v3_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3_smem_bytes<2>());
+        stencil_v3_kernel<2, 0><<<grid, block, v3_smem_bytes<2>(), st>>>(a, iper);
+      } else {
+        cudaFuncSetAttribute(stencil_v3_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3_smem_bytes<2>());
+        stencil_v3_kernel<2, 1><<<grid, block, v3_smem_bytes<2>(), st>>>(a, iper);
+      }
     } else {
-      cudaFuncSetAttribute(stencil_v3_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3_smem_bytes<4>());
-      stencil_v3_kernel<4><<<grid, block, v3_smem_bytes<4>(), st>>>(a, iper);
+      if (a.vel_kind == 0) {
+        cudaFuncSetAttribute(stencil_v3_kernel<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3_smem_bytes<4>());
+        stencil_v3_kernel<4, 0><<<grid, block, v3_smem_bytes<4>(), st>>>(a, iper);
+      } else {
+        cudaFuncSetAttribute(stencil_v3_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v3_smem_bytes<4>());
+        stencil_v3_kernel<4, 1><<<grid, block, v3_smem_bytes<4>(), st>>>(a, iper);
+      }
     }
     return cudaGetLastError();
   }
