@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(kV2Threads, (kV2Threads <= 256 ? 2 : 1)) stenc
 }
 
 #ifndef MR_V3_TJ
-#define MR_V3_TJ 16
+#define MR_V3_TJ 8  // 16 rows x 1 block/SM: 62.4%; 8 rows x 2 blocks/SM: 63.4% (256^3), 48 -> 53% (128^3)
 #endif
 #ifndef MR_V3_PF
 #define MR_V3_PF 4
@@ -486,7 +486,7 @@ constexpr size_t v3_smem_bytes()
 // ring is synchronised by per-slot full/empty mbarriers (MR_V3_MBAR): no block
 // barrier in the march, so warps drift up to two planes apart.
 template <int M, int VK>
-__global__ void __launch_bounds__(kV3Block, 1) stencil_v3_kernel(const StencilArgs a, int iper)
+__global__ void __launch_bounds__(kV3Block, kV3Threads <= 128 ? 2 : 1) stencil_v3_kernel(const StencilArgs a, int iper)
 {
   constexpr int PF = kV3PF;
   constexpr int RJ = kV3TJ + 2 * M, RK = kV2TK + 2 * M, R = M + PF + 1;
