@@ -101,6 +101,7 @@ struct ChemCfg {
   int NW, SPL;  // warps per cell group (slots), components per thread
   int NG;       // cell groups (of 32 cells) per block, named barriers per group
   bool subdiag;
+  int nstage;  // inner table stages (non-subdiagonal tables: stage accumulators)
   int ndeg;
 };
 

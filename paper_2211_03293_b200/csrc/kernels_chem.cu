@@ -22,6 +22,8 @@ MR_DECL(16, 4)
 MR_DECL(24, 3)
 MR_DECL(32, 2)
 #undef MR_DECL
+extern template cudaError_t run_chem_chain<32, 2, false, 3, 1>(const ChainArgs&, const ChemParams&, cudaStream_t);
+extern template cudaError_t run_chem_chain<32, 2, false, 3, 2>(const ChainArgs&, const ChemParams&, cudaStream_t);
 #define MR_DECL_G(A, B, G)                                                                      \
   extern template cudaError_t run_chem_chain<A, B, true, 4, 1, G>(const ChainArgs&, const ChemParams&, cudaStream_t);  \
   extern template cudaError_t run_chem_chain<A, B, true, 4, 2, G>(const ChainArgs&, const ChemParams&, cudaStream_t);  \
@@ -43,6 +45,7 @@ int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int nd
     for (int j = 0; j < i - 1; ++j)
       if (tab.A[i][j] != 0.0) subdiag = false;
   cfg->subdiag = subdiag;
+  cfg->nstage = tab.s;
   cfg->ndeg = ndeg;
   cfg->NG = 1;
   if (ncomp <= 12) { cfg->NW = 4; cfg->SPL = 3; }
@@ -95,6 +98,10 @@ cudaError_t launch_chem_chain(const ChemCfg& cfg, const ChainArgs& a, const Chem
     if (cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem_chain<A, B, true, 4, 2>(a, P, st);   \
     if (!cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem_chain<A, B, false, 6, 1>(a, P, st); \
     if (!cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem_chain<A, B, false, 6, 2>(a, P, st); \
+  }
+  if (cfg.NW == 32 && cfg.SPL == 2 && cfg.NG == 1 && !cfg.subdiag && cfg.nstage <= 3) {
+    if (cfg.ndeg == 1) return mrchem::run_chem_chain<32, 2, false, 3, 1>(a, P, st);
+    if (cfg.ndeg == 2) return mrchem::run_chem_chain<32, 2, false, 3, 2>(a, P, st);
   }
   MR_CHEM_BLOCK_LAYOUTS(MR_CHEM_DISPATCH)
 #undef MR_CHEM_DISPATCH

@@ -7,5 +7,8 @@ template cudaError_t run_chem_chain<32, 2, true, 4, 1>(const ChainArgs&, const C
 template cudaError_t run_chem_chain<32, 2, true, 4, 2>(const ChainArgs&, const ChemParams&, cudaStream_t);
 template cudaError_t run_chem_chain<32, 2, false, 6, 1>(const ChainArgs&, const ChemParams&, cudaStream_t);
 template cudaError_t run_chem_chain<32, 2, false, 6, 2>(const ChainArgs&, const ChemParams&, cudaStream_t);
+// three-stage non-subdiagonal tables (kutta3, C5): fewer stage accumulators
+template cudaError_t run_chem_chain<32, 2, false, 3, 1>(const ChainArgs&, const ChemParams&, cudaStream_t);
+template cudaError_t run_chem_chain<32, 2, false, 3, 2>(const ChainArgs&, const ChemParams&, cudaStream_t);
 template cudaError_t run_chem_rhs<32, 2>(const double*, double*, size_t, int, const ChemParams&, cudaStream_t);
 }  // namespace mrchem
