@@ -269,40 +269,14 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
   }
   grp_sync<NG>(g, NW * 32);
   MR_PH(1);  // energy partial sums
-#ifndef MR_TSUM_TREE
-#define MR_TSUM_TREE 1
-#endif
   if (w == 0) {
     double E0 = 0.0, E1 = 0.0, E2 = 0.0, ee = 0.0;
-#if MR_TSUM_TREE
-    if constexpr (NW % 4 == 0 && NW >= 8) {
-      // four interleaved chains per quantity (dependent-add latency / 4),
-      // combined as (a + b) + (c + d): a fixed order, deterministic
-      double a4[4][4];
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) a4[x][u] = 0.0;
-#pragma unroll
-      for (int q = 0; q < NW / 4; ++q)
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int x = 0; x < 4; ++x) a4[x][u] += m.part[(x * NW + u * (NW / 4) + q) * 32 + c];
-      E0 = (a4[0][0] + a4[0][1]) + (a4[0][2] + a4[0][3]);
-      E1 = (a4[1][0] + a4[1][1]) + (a4[1][2] + a4[1][3]);
-      E2 = (a4[2][0] + a4[2][1]) + (a4[2][2] + a4[2][3]);
-      ee = (a4[3][0] + a4[3][1]) + (a4[3][2] + a4[3][3]);
-    } else
-#endif
-    {
-#pragma unroll
-      for (int q = 0; q < NW; ++q) {
-        E0 += m.part[(0 * NW + q) * 32 + c];
-        E1 += m.part[(1 * NW + q) * 32 + c];
-        E2 += m.part[(2 * NW + q) * 32 + c];
-        ee += m.part[(3 * NW + q) * 32 + c];
-      }
+    for (int q = 0; q < NW; ++q) {
+      E0 += m.part[(0 * NW + q) * 32 + c];
+      E1 += m.part[(1 * NW + q) * 32 + c];
+      E2 += m.part[(2 * NW + q) * 32 + c];
+      ee += m.part[(3 * NW + q) * 32 + c];
     }
     const double de = ee - E0;
     const double T = (2.0 * de) / (E1 + sqrt(E1 * E1 + 4.0 * E2 * de));
