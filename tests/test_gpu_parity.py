@@ -115,6 +115,19 @@ def test_slow_rhs_tiled_kernel_matches_oracle(name, n):
     assert per_species_rel_err(got, ref, cfg["S"] + 1) <= RHS_TOL
 
 
+@pytest.mark.parametrize("u", [(1.0, -0.5, 0.25), (0.0, 0.0, 0.0)])
+def test_slow_rhs_order8_uniform_velocity(u):
+    """Order 8 with a uniform velocity on a grid the ring kernel tiles (the
+    compile-time uniform-velocity instantiation; C3/C4 use the profile one)."""
+    n = 64
+    cfg = dict(CONFIGS["C3"], velocity="uniform", u=u)
+    ctx = P.Context(0)
+    cfg, y0 = P.setup_workload(ctx, "C3", n=n, config=cfg)
+    ref = oracle_physics(cfg, n).slow_rhs(y0)
+    got = ctx.slow_rhs(y0)
+    assert per_species_rel_err(got, ref, cfg["S"] + 1) <= RHS_TOL
+
+
 def test_slow_rhs_properties():
     """test_models.cpp:126-232 ported to 3D: constant -> 0, per-species
     telescoping conservation, linearity."""
