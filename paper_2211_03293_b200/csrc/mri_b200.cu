@@ -325,7 +325,7 @@ int ensure_halo(mr_ctx* c)
   free_dev_t(c->recv_hi);
   MR_CUDA_TRY(c, cudaMalloc(&c->send_lo, need * sizeof(double)));
   MR_CUDA_TRY(c, cudaMalloc(&c->send_hi, need * sizeof(double)));
-  if (c->nranks > 1) {
+  if (c->comm) {
     MR_CUDA_TRY(c, cudaMalloc(&c->recv_lo, need * sizeof(double)));
     MR_CUDA_TRY(c, cudaMalloc(&c->recv_hi, need * sizeof(double)));
   }
@@ -546,7 +546,7 @@ int exchange_halos(mr_ctx** cs, int n, const double* const* ycur, const double**
                                     c->M, st));
     c->launches++;
   }
-  if (n == 1 && cs[0]->nranks == 1) {  // periodic single slab: own planes wrap around
+  if (n == 1 && !cs[0]->comm) {  // periodic single slab: own planes wrap around
     lo[0] = cs[0]->send_hi;
     hi[0] = cs[0]->send_lo;
     return MR_OK;
@@ -754,7 +754,7 @@ int dot_finalize(mr_ctx** cs, int n, int slot, cudaStream_t st, bool second = fa
     for (int r = 0; r < n; ++r) scs[r] = cs[r]->cg_sc;
     MR_CUDA_TRY(cs[0], launch_scalar_combine(scs.data(), n, slot, st));
     cs[0]->launches++;
-  } else if (cs[0]->nranks > 1) {
+  } else if (cs[0]->comm) {
     mr_ctx* c = cs[0];
     MR_NCCL_TRY(c, AllGather(c->cg_sc + slot, c->cg_gather, 1, ncclDouble, c->comm, st));
     MR_CUDA_TRY(c, launch_gathered_sum(c->cg_gather, c->nranks, c->cg_sc, slot, st));
@@ -1004,7 +1004,7 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
 
   // combine failure keys (min over slabs / ranks)
   unsigned long long key = MR_NO_FAIL;
-  if (n == 1 && c0->nranks > 1) {
+  if (n == 1 && c0->comm) {
     MR_NCCL_TRY(c0, AllReduce(c0->d_fail, c0->d_fail, 1, ncclUint64, ncclMin, c0->comm, st));
   }
   for (int r = 0; r < n; ++r) {
@@ -1808,7 +1808,7 @@ int ark_domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, 
     }
   }
   unsigned long long key = MR_NO_FAIL;
-  if (n == 1 && c0->nranks > 1)
+  if (n == 1 && c0->comm)
     MR_NCCL_TRY(c0, AllReduce(c0->d_fail, c0->d_fail, 1, ncclUint64, ncclMin, c0->comm, st));
   for (int r = 0; r < n; ++r)
     MR_CUDA_TRY(cs[r], cudaMemcpyAsync(cs[r]->h_fail, cs[r]->d_fail, sizeof(unsigned long long),
@@ -2055,7 +2055,7 @@ static int erk_integrate_dev(mr_ctx* c, int s, const double* A, const double* b,
       MR_CUDA_TRY(c, launch_update(c->y_state, c->y_work, nref, f, cf, c->dof, s, c->d_fail, st));
       c->launches++;
     }
-    if (c->nranks > 1)
+    if (c->comm)
       MR_NCCL_TRY(c, AllReduce(c->d_fail, c->d_fail, 1, ncclUint64, ncclMin, c->comm, st));
     MR_CUDA_TRY(c, cudaMemcpyAsync(c->h_fail, c->d_fail, sizeof(unsigned long long),
                                    cudaMemcpyDeviceToHost, st));
@@ -2202,7 +2202,11 @@ int mr_comm_init(mr_ctx* c, int nranks, int rank, const char* id128)
 {
   if (!c || nranks < 1 || rank < 0 || rank >= nranks || !id128) return MR_CONTRACT;
   cudaSetDevice(c->device);
-  if (nranks == 1) {
+  // nranks == 1: no communicator, the periodic single-slab path -- unless
+  // MR_NCCL_SELF is set, which builds a one-rank NCCL communicator so the whole
+  // NCCL path (halo send/recv to itself, failure-key all-reduce, all-gathered
+  // CG dot products) runs on one GPU (tests compare it with the plain path)
+  if (nranks == 1 && !getenv("MR_NCCL_SELF")) {
     c->nranks = 1;
     c->rank = 0;
     return MR_OK;
@@ -2220,7 +2224,7 @@ int mr_group_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, in
 {
   if (!cs || n < 1) return MR_CONTRACT;
   for (int r = 0; r < n; ++r)
-    if (!cs[r] || cs[r]->device != cs[0]->device || cs[r]->nranks != 1)
+    if (!cs[r] || cs[r]->device != cs[0]->device || cs[r]->nranks != 1 || cs[r]->comm)
       return set_err(cs[0], MR_CONTRACT, "mr_group_step: contexts must share one device");
   cudaSetDevice(cs[0]->device);
   // order all slabs on the first context's stream

@@ -1,0 +1,63 @@
+"""The NCCL path of the slab decomposition on one GPU: a one-rank NCCL
+communicator (MR_NCCL_SELF) sends the halo planes to itself with grouped
+ncclSend/ncclRecv, all-reduces the failure key and all-gathers the CG dot
+products -- every collective the multi-GPU run issues.  Its
+results must equal the plain single-slab path bit for bit (same data, same
+order), and its counters exactly."""
+import numpy as np
+import pytest
+
+import paper_2211_03293_b200 as P
+from paper_2211_03293_b200.configs import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(monkeypatch, name, n, cfg):
+    plain = P.Context(0)
+    P.setup_workload(plain, name, n=n, config=cfg)
+    nccl = P.Context(0)
+    monkeypatch.setenv("MR_NCCL_SELF", "1")
+    nccl.comm_init(1, 0, P.Context.nccl_unique_id())
+    monkeypatch.delenv("MR_NCCL_SELF")
+    cfg_, y0 = P.setup_workload(nccl, name, n=n, config=cfg)
+    return plain, nccl, cfg_, y0
+
+
+def test_nccl_self_explicit_steps_bitwise(monkeypatch):
+    """C3 physics (8th-order stencil with halo exchange, chemistry chains)."""
+    plain, nccl, cfg, _ = _pair(monkeypatch, "C3", 16, dict(CONFIGS["C3"]))
+    H = cfg["H"]
+    c_a = plain.mri_integrate(0.0, 2 * H, H)
+    c_b = nccl.mri_integrate(0.0, 2 * H, H)
+    assert np.array_equal(c_a, c_b)
+    assert np.array_equal(plain.download(), nccl.download())
+
+
+def test_nccl_self_imex_newton_pcg_bitwise(monkeypatch):
+    """C5 physics with a transport-scale H: Newton iterates, every CG dot
+    product goes through ncclAllGather + the fixed-order sum."""
+    cfg0 = dict(CONFIGS["C5"], d_impl=0.05, cg_iters=3, m=4)
+    plain, nccl, cfg, _ = _pair(monkeypatch, "C5", 12, cfg0)
+    plain.fast_none()
+    nccl.fast_none()
+    H = 2e-3
+    c_a = plain.mri_integrate(0.0, 2 * H, H)
+    c_b = nccl.mri_integrate(0.0, 2 * H, H)
+    assert np.array_equal(c_a, c_b)
+    assert c_a[4] > c_a[3]  # Newton iterated (linear iterations > solves)
+    assert np.array_equal(plain.download(), nccl.download())
+
+
+def test_nccl_self_failure_key_allreduce(monkeypatch):
+    """A blow-up is reported with the same stage through the all-reduced key."""
+    plain, nccl, cfg, y0 = _pair(monkeypatch, "C3", 16, dict(CONFIGS["C3"]))
+    bad = y0.copy()
+    bad[5] = np.nan
+    errs = []
+    for ctx in (plain, nccl):
+        ctx.upload(bad)
+        with pytest.raises(P.IntegrationError) as e:
+            ctx.mri_step(0.0, cfg["H"])
+        errs.append(e.value.stage_index)
+    assert errs[0] == errs[1]
