@@ -185,6 +185,12 @@ int mr_max_norm_component(mr_ctx* ctx, const double* x, size_t n, size_t offset,
 int mr_all_finite(mr_ctx* ctx, const double* x, size_t n, int* out);
 
 /* ---------------- multi-GPU (slab decomposition over NCCL) ---------------- */
+/* id128: ncclUniqueId bytes from rank 0 (broadcast by the caller).  Call before
+ * mr_grid_set; the context then owns the slab [i0, i0 + n0_local) of its rank and
+ * exchanges g = order/2 ghost planes per slow evaluation with grouped
+ * ncclSend/ncclRecv.  nranks == 1 builds no communicator (periodic single slab)
+ * unless the environment sets MR_NCCL_SELF, which builds a one-rank
+ * communicator so the NCCL path can be exercised on one GPU. */
 int mr_nccl_unique_id(char* id128);
 int mr_comm_init(mr_ctx* ctx, int nranks, int rank, const char* id128);
 
