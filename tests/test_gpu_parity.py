@@ -413,3 +413,38 @@ def test_virtual_rank_slabs_equal_single_gpu_bitwise(P_, n):
     for r, c in enumerate(ctxs):
         i0, n0l = P.slab_bounds(n, P_, r)
         assert np.array_equal(c.download().reshape(cfg["S"] + 1, n0l, n, n), ref[:, i0:i0 + n0l])
+
+
+# ------------------------------------------------- host-buffer step (e2e ABI)
+@pytest.mark.parametrize("name,n", [("C3", 16), ("C4", 8), ("C1", 12)])
+def test_host_buffer_step_equals_device_step(name, n):
+    """mr_mri_step_host (pinned or pageable host buffers, H2D + step + D2H)
+    returns exactly the device-resident step's state and counters."""
+    import torch
+    dev, cfg, y0 = gpu_ctx(name, n)
+    c_dev = dev.mri_step(0.0, cfg["H"])
+    ref = dev.download()
+    host, _, _ = gpu_ctx(name, n)
+    y_in = torch.from_numpy(y0.copy()).pin_memory().numpy()
+    y_out = torch.zeros(y0.size, dtype=torch.float64).pin_memory().numpy()
+    c_host = host.counters()
+    host.mri_step_host(0.0, cfg["H"], y_in, y_out, c_host)
+    assert np.array_equal(c_host, c_dev)
+    assert np.array_equal(y_out, ref)
+    y_pageable = np.zeros_like(y0)  # pageable destination: same result
+    host.mri_step_host(0.0, cfg["H"], y0, y_pageable)
+    assert np.array_equal(y_pageable, ref)
+
+
+def test_host_buffer_step_failure_keeps_input():
+    """A failing host-buffer step raises the reference's IntegrationError and
+    writes nothing to y_out (no partial result); the device state is the
+    input, as the reference's mri_integrate keeps y on a throw."""
+    ctx, cfg, y0 = gpu_ctx("C3", 16)
+    bad = y0.copy()
+    bad[7] = np.nan
+    y_out = np.full_like(y0, 3.0)
+    with pytest.raises(P.IntegrationError):
+        ctx.mri_step_host(0.0, cfg["H"], bad, y_out)
+    assert np.all(y_out == 3.0)
+    assert np.array_equal(ctx.download(), bad, equal_nan=True)
