@@ -320,6 +320,11 @@ def run_ours(args):
         threads = os.cpu_count() or 1
         r = cpu_reference_sample(args.config, args.sample_n, 1, threads)
         cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        # the reference is single-threaded by design (proj/README.md:132-134):
+        # also time it on one host thread, on a smaller sub-grid
+        n1 = max(6, args.sample_n // 2)
+        r1 = cpu_reference_sample(args.config, n1, 1, 1)
+        cpu["single_thread"] = {k: r1[k] for k in ("value", "unit", "cores", "sample")}
 
     if rank == 0:
         line = {
