@@ -219,6 +219,17 @@ def step_counts(coupling: str, fast_table: str, m: int, fast=True, slow=True):
 
 
 # --------------------------------------------------------------------------
+def _bind_process_nccl():
+    """The library resolves NCCL lazily and binds to the libnccl.so.2 already in
+    the process (csrc/nccl_shim.h).  Import torch first when it is installed so
+    that is PyTorch's bundled NCCL: binding the system NCCL first would leave
+    a later `import torch` with unresolved NCCL symbols."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 class Context:
     """One device-resident MRI problem (one slab of the grid)."""
 
@@ -490,12 +501,14 @@ class Context:
     # ---- multi-GPU -----------------------------------------------------------
     @staticmethod
     def nccl_unique_id() -> bytes:
+        _bind_process_nccl()
         buf = C.create_string_buffer(128)
         if lib().mr_nccl_unique_id(buf):
             raise CudaError("ncclGetUniqueId failed")
         return buf.raw
 
     def comm_init(self, nranks, rank, uid: bytes):
+        _bind_process_nccl()
         self._check(self.L.mr_comm_init(self.h, nranks, rank, uid))
 
 

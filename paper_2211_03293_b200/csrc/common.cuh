@@ -118,6 +118,7 @@ struct StencilArgs {
   const double* halo_hi;  // [comp][g][n1*n2]: planes i0+n0l .. i0+n0l+g-1
   int n0l, n1, n2, ncomp, M;
   int i0;                 // global index of the first local plane
+  int i_lo, i_hi;         // local planes [i_lo, i_hi) this launch writes (ring kernel; others: all)
   double a[5], b[5];
   double inv_dx[3], inv_dx2[3];
   double D;
@@ -176,6 +177,7 @@ cudaError_t launch_update(const double* y_in, double* y_out, int nref, const dou
                           const double* coef, size_t n, int mri_stage,
                           unsigned long long* fail, cudaStream_t st);
 cudaError_t launch_stencil(const StencilArgs& a, cudaStream_t st);
+bool stencil_plane_ranges(const StencilArgs& a);  // launch_stencil accepts [i_lo, i_hi) < all planes
 cudaError_t launch_slow_linear(const double* y, double* out, size_t ncell, const LinDev& lin,
                                cudaStream_t st);
 cudaError_t launch_halo_pack(const double* y, double* send_lo, double* send_hi, int ncomp,

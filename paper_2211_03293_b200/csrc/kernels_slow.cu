@@ -494,10 +494,10 @@ __global__ void __launch_bounds__(kV3Block, kV3Threads <= 128 ? 2 : 1) stencil_v
   extern __shared__ __align__(16) double ring[];  // [R][RJ][RK]
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
   const int k0 = blockIdx.x * kV2TK, j0 = blockIdx.y * kV3TJ;
-  const int nchunk = (a.n0l + iper - 1) / iper;
+  const int nchunk = (a.i_hi - a.i_lo + iper - 1) / iper;
   const int comp = blockIdx.z / nchunk;
-  const int ib = (blockIdx.z % nchunk) * iper;
-  const int ie = min(a.n0l, ib + iper);
+  const int ib = a.i_lo + (blockIdx.z % nchunk) * iper;
+  const int ie = min(a.i_hi, ib + iper);
   const int n0l = a.n0l, n1 = a.n1, n2 = a.n2;
   const size_t plane = (size_t)n1 * n2;
   const size_t ncell = plane * n0l;
@@ -953,16 +953,26 @@ __global__ void fp64_peak_kernel(double* sink, int iters)
 
 }  // namespace
 
+bool stencil_plane_ranges(const StencilArgs& a)
+{
+  static const bool v2 = getenv("MR_STENCIL_V1") == nullptr;  // A/B hook
+  return v2 && a.M == 4 && a.n1 % kV3TJ == 0 && a.n2 % kV2TK == 0;
+}
+
 cudaError_t launch_stencil(const StencilArgs& a, cudaStream_t st)
 {
   const size_t ncell = (size_t)a.n0l * a.n1 * a.n2;
   static const bool v2 = getenv("MR_STENCIL_V1") == nullptr;  // A/B hook
-  if (v2 && a.M == 4 && a.n1 % kV3TJ == 0 && a.n2 % kV2TK == 0) {
+  const bool full = a.i_lo == 0 && a.i_hi == a.n0l;
+  if (!full && !stencil_plane_ranges(a)) return cudaErrorInvalidValue;
+  if (a.i_hi <= a.i_lo) return cudaSuccess;
+  if (stencil_plane_ranges(a)) {
+    const int span = a.i_hi - a.i_lo;
     const size_t tiles = (size_t)(a.n1 / kV3TJ) * (a.n2 / kV2TK) * a.ncomp;
-    int iper = a.n0l;
-    while (iper > 16 && tiles * ((a.n0l + iper - 1) / iper) < 148 * 8) iper = (iper + 1) / 2;
+    int iper = span;
+    while (iper > 16 && tiles * ((span + iper - 1) / iper) < 148 * 8) iper = (iper + 1) / 2;
     while (iper > kV3MaxPlanes) iper = (iper + 1) / 2;
-    const unsigned nch = (unsigned)((a.n0l + iper - 1) / iper);
+    const unsigned nch = (unsigned)((span + iper - 1) / iper);
     dim3 grid(a.n2 / kV2TK, a.n1 / kV3TJ, (unsigned)a.ncomp * nch);
     dim3 block(32, kV3Block / 32);
     if (a.M == 1) {

@@ -211,6 +211,8 @@ struct mr_ctx {
   // comm
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
+  cudaStream_t comm_stream = nullptr;  // halo exchange overlapped with the interior stencil
+  cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
   // instrumentation
   uint64_t launches = 0;
   bool profile = false;
@@ -532,6 +534,21 @@ cudaEvent_t pool_event(mr_ctx* c, size_t idx)
   return c->ev_pool[idx];
 }
 
+// grouped send/recv of the packed ghost planes with the periodic neighbours
+// (r - 1) mod P and (r + 1) mod P (a one-rank communicator sends to itself)
+int nccl_halo_exchange(mr_ctx* c, cudaStream_t st)
+{
+  const int left = (c->rank - 1 + c->nranks) % c->nranks;
+  const int right = (c->rank + 1) % c->nranks;
+  MR_NCCL_TRY(c, GroupStart());
+  MR_NCCL_TRY(c, Send(c->send_lo, c->halo_elems, ncclDouble, left, c->comm, st));
+  MR_NCCL_TRY(c, Recv(c->recv_hi, c->halo_elems, ncclDouble, right, c->comm, st));
+  MR_NCCL_TRY(c, Send(c->send_hi, c->halo_elems, ncclDouble, right, c->comm, st));
+  MR_NCCL_TRY(c, Recv(c->recv_lo, c->halo_elems, ncclDouble, left, c->comm, st));
+  MR_NCCL_TRY(c, GroupEnd());
+  return MR_OK;
+}
+
 // ---------------------------------------------------------------------------
 // halo exchange for the stencil: fills halo pointers of every context
 // ---------------------------------------------------------------------------
@@ -553,14 +570,8 @@ int exchange_halos(mr_ctx** cs, int n, const double* const* ycur, const double**
   }
   if (n == 1) {  // NCCL ring of slabs
     mr_ctx* c = cs[0];
-    const int left = (c->rank - 1 + c->nranks) % c->nranks;
-    const int right = (c->rank + 1) % c->nranks;
-    MR_NCCL_TRY(c, GroupStart());
-    MR_NCCL_TRY(c, Send(c->send_lo, c->halo_elems, ncclDouble, left, c->comm, st));
-    MR_NCCL_TRY(c, Recv(c->recv_hi, c->halo_elems, ncclDouble, right, c->comm, st));
-    MR_NCCL_TRY(c, Send(c->send_hi, c->halo_elems, ncclDouble, right, c->comm, st));
-    MR_NCCL_TRY(c, Recv(c->recv_lo, c->halo_elems, ncclDouble, left, c->comm, st));
-    MR_NCCL_TRY(c, GroupEnd());
+    int rc = nccl_halo_exchange(c, st);
+    if (rc) return rc;
     lo[0] = c->recv_lo;
     hi[0] = c->recv_hi;
     return MR_OK;
@@ -601,6 +612,8 @@ StencilArgs stencil_args(const mr_ctx* c, const double* y, double* out, const do
   a.ncomp = c->ncomp;
   a.M = c->M;
   a.i0 = c->i0;
+  a.i_lo = 0;
+  a.i_hi = c->n0l;
   for (int i = 0; i < 5; ++i) a.a[i] = a.b[i] = 0.0;
   if (c->order == 2) {
     a.a[1] = 1.0 / 2.0;
@@ -637,6 +650,44 @@ int eval_slow(mr_ctx** cs, int n, const double* const* ycur, double* const* outs
       cs[r]->launches++;
     }
     return MR_OK;
+  }
+  if (n == 1 && cs[0]->comm) {
+    // NCCL rank: the halo exchange runs on the comm stream while the interior
+    // planes [M, n0l - M) -- which read no ghost plane -- are computed; the
+    // boundary planes follow once the halos have landed
+    mr_ctx* c = cs[0];
+    StencilArgs a = stencil_args(c, ycur[0], outs[0], nullptr, nullptr);
+    if (stencil_plane_ranges(a) && c->n0l >= 2 * c->M + 1) {
+      int rc = ensure_halo(c);
+      if (rc) return rc;
+      if (!c->comm_stream) {
+        MR_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+        MR_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming));
+        MR_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+      }
+      MR_CUDA_TRY(c, launch_halo_pack(ycur[0], c->send_lo, c->send_hi, c->ncomp, c->n0l, c->plane,
+                                      c->M, st));
+      c->launches++;
+      MR_CUDA_TRY(c, cudaEventRecord(c->ev_pack, st));
+      MR_CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_pack, 0));
+      rc = nccl_halo_exchange(c, c->comm_stream);
+      if (rc) return rc;
+      MR_CUDA_TRY(c, cudaEventRecord(c->ev_halo, c->comm_stream));
+      a.halo_lo = c->recv_lo;
+      a.halo_hi = c->recv_hi;
+      a.i_lo = c->M;
+      a.i_hi = c->n0l - c->M;
+      MR_CUDA_TRY(c, launch_stencil(a, st));  // interior
+      MR_CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
+      a.i_lo = 0;
+      a.i_hi = c->M;
+      MR_CUDA_TRY(c, launch_stencil(a, st));  // first ghost-dependent planes
+      a.i_lo = c->n0l - c->M;
+      a.i_hi = c->n0l;
+      MR_CUDA_TRY(c, launch_stencil(a, st));  // last ghost-dependent planes
+      c->launches += 3;
+      return MR_OK;
+    }
   }
   std::vector<const double*> lo(n), hi(n);
   int rc = exchange_halos(cs, n, ycur, lo.data(), hi.data(), st);
@@ -1172,6 +1223,9 @@ void mr_ctx_destroy(mr_ctx* c)
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->comm && nccl_api().ok) nccl_api().CommDestroy(c->comm);
   cudaStreamDestroy(c->stream);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->ev_pack) cudaEventDestroy(c->ev_pack);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
   delete c;
 }
 

@@ -61,3 +61,20 @@ def test_nccl_self_failure_key_allreduce(monkeypatch):
             ctx.mri_step(0.0, cfg["H"])
         errs.append(e.value.stage_index)
     assert errs[0] == errs[1]
+
+
+def test_nccl_self_overlapped_halo_bitwise(monkeypatch):
+    """On a grid the ring stencil tiles (64^3, order 8) the NCCL rank overlaps
+    the halo exchange (comm stream) with the interior planes and finishes the
+    ghost-dependent planes after it: still bitwise equal to the plain path."""
+    plain, nccl, cfg, y0 = _pair(monkeypatch, "C3", 64, dict(CONFIGS["C3"]))
+    H = cfg["H"]
+    n_before = nccl.launch_count()
+    c_a = plain.mri_step(0.0, H)
+    c_b = nccl.mri_step(0.0, H)
+    assert np.array_equal(c_a, c_b)
+    assert np.array_equal(plain.download(), nccl.download())
+    # the stencil evaluations ran as interior + two boundary launches
+    assert nccl.launch_count() - n_before > plain.launch_count()
+    # slow RHS alone (through the same path as a step's evaluations)
+    assert np.array_equal(plain.slow_rhs(y0), nccl.slow_rhs(y0))
