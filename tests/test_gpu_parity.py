@@ -242,6 +242,25 @@ def test_linear_bitwise_vs_reference(cp, table, H):
     assert np.array_equal(cnt, FIX[f"lin_{cp}_{H}_counters"])
 
 
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("cp,table,tf,H", [("mis-kw3", "bogacki-shampine3", 1.0, 0.3),
+                                           ("imex-mri-gark4-explicit", "classic-rk4", 0.77, 0.1)])
+def test_linear_short_last_step_bitwise_vs_reference(cp, table, tf, H):
+    """tf not a multiple of H: n_steps = ceil((tf - t0)/H - 1e-12), the last
+    step is tf - t and t = t0 + (i+1) H (mri.cpp:524-540) -- bit-identical to
+    the reference's own mri_integrate run live from oracle/_ref."""
+    m = 7
+    ctx = lin_ctx(cp, table, m, ncell=1)
+    ctx.upload(Y0_LIN)
+    cnt = ctx.mri_integrate(0.0, tf, H)
+    sysm = O.System(1, 1, 1, 2, fast="linear", slow="linear", fast_A=A_FAST,
+                    slow_A=np.asarray(A_SI) + np.asarray(A_SE))
+    y_ref, cnt_ref = sysm.mri_integrate(P.coupling_text(cp), table, m, 0.0, tf, H,
+                                        np.asarray(Y0_LIN, dtype=np.float64), use_reference=True)
+    assert np.array_equal(ctx.download(), y_ref)
+    assert np.array_equal(cnt, cnt_ref)
+
+
 def test_rk4_taylor_known_answer():
     """test_erk.cpp:35-42: one classic-rk4 step of y'=y, h=0.1 gives the
     degree-4 Taylor polynomial 1.1051708333333333 -- through a one-IVP coupling."""
