@@ -706,7 +706,9 @@ __global__ void __launch_bounds__(kV3Block, kV3Threads <= 128 ? 2 : 1) stencil_v
       ready(i + M);
 #pragma unroll
       for (int e = 0; e < 2; ++e) pair(tq, jl + e, kl, qv[2 * e][(ph + 2 * M) % Q], qv[2 * e + 1][(ph + 2 * M) % Q]);
+#if !MR_V3_HOIST
       const int ig = a.i0 + i;
+#endif
       double cadv1[2], cadv2[2];  // u_1 depends on (i, k), u_2 on (i, j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
@@ -1009,7 +1011,6 @@ cudaError_t launch_stencil(const StencilArgs& a, cudaStream_t st)
     const unsigned nch = (unsigned)((a.n0l + iper - 1) / iper);
     dim3 grid(a.n2 / kV2TK, a.n1 / kV2TJ, (unsigned)a.ncomp * nch);
     dim3 block(32, kV2Threads / 32);
-    cudaError_t e = cudaSuccess;
     if (a.M == 1) {
       cudaFuncSetAttribute(stencil_v2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v2_smem_bytes<1>());
       stencil_v2_kernel<1><<<grid, block, v2_smem_bytes<1>(), st>>>(a, iper);
@@ -1020,7 +1021,6 @@ cudaError_t launch_stencil(const StencilArgs& a, cudaStream_t st)
       cudaFuncSetAttribute(stencil_v2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v2_smem_bytes<4>());
       stencil_v2_kernel<4><<<grid, block, v2_smem_bytes<4>(), st>>>(a, iper);
     }
-    (void)e;
     return cudaGetLastError();
   }
   if (a.n1 % kTY == 0 && a.n2 % kTX == 0 && a.n1 >= kTY && a.n2 >= kTX) {
