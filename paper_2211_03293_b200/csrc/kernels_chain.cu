@@ -34,6 +34,14 @@ namespace {
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+// (used by the generic kernel's chemistry branch, instantiated only when the
+// block chemistry kernel cannot take a mechanism)
+[[maybe_unused]] __device__ __forceinline__ double4 ldg4(const double4* p)
+{
+  const double2 lo = __ldg(reinterpret_cast<const double2*>(p));
+  const double2 hi = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(lo.x, lo.y, hi.x, hi.y);
+}
 
 // ---------------------------------------------------------------------------
 // Per-cell synthetic Arrhenius chemistry (CPU form in
