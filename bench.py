@@ -198,6 +198,13 @@ def run_ours(args):
         uid = [P.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.comm_init(world, rank, uid[0])
+    elif args.nccl_self:
+        # one-rank NCCL communicator: the multi-GPU rank's code path (pack,
+        # grouped send/recv on the comm stream overlapped with the interior
+        # stencil, boundary planes, all-reduced failure key) on one GPU
+        os.environ["MR_NCCL_SELF"] = "1"
+        ctx.comm_init(1, 0, P.Context.nccl_unique_id())
+        del os.environ["MR_NCCL_SELF"]
     t_setup = time.perf_counter()
     cfg, y0 = P.setup_workload(ctx, args.config, n=n, i0=i0, n0_local=n0l, threads=0)
     if cfg.get("d_impl") is not None and dist:
@@ -335,7 +342,8 @@ def run_ours(args):
             "config": {"workload": workload_text(args, cfg, n, n0l, H),
                        "grid": n, "species": S, "reactions": cfg["R"],
                        "parallelism": f"slab{world}" if world > 1 else (
-                           f"single GPU, slab 1/{args.slab_of}" if args.slab_of else "single GPU"),
+                           (f"single GPU, slab 1/{args.slab_of}" if args.slab_of else "single GPU")
+                           + (", one-rank NCCL path" if args.nccl_self else "")),
                        "l2": (f"inputs > L2 ({8 * (S + 1) * ncell_local / 1e9:.2f} GB state "
                               f"per GPU)") if 8 * (S + 1) * ncell_local > 126e6 else "fits L2"},
             "chem_rhs_cells_per_s": chem_cells_per_s,
@@ -403,6 +411,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--nccl-self", action="store_true",
+                    help="N=1: run the NCCL rank path through a one-rank communicator")
     ap.add_argument("--slab-of", type=int, default=0,
                     help="N=1: run one rank's slab of an N-GPU decomposition (e.g. C5: 8)")
     args = ap.parse_args()
