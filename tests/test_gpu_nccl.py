@@ -78,3 +78,20 @@ def test_nccl_self_overlapped_halo_bitwise(monkeypatch):
     assert nccl.launch_count() - n_before > plain.launch_count()
     # slow RHS alone (through the same path as a step's evaluations)
     assert np.array_equal(plain.slow_rhs(y0), nccl.slow_rhs(y0))
+
+
+def test_bench_nccl_self_line():
+    """bench.py --nccl-self (a multi-GPU rank's code path on one GPU) prints a
+    valid contract line."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "C3", "--n", "64",
+                          "--steps", "1", "--warmup", "1", "--no-cpu", "--no-e2e", "--nccl-self"],
+                         capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert "one-rank NCCL path" in line["config"]["parallelism"]
+    assert line["value"] > 0 and line["gpu_launches"] > 0
