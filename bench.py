@@ -347,7 +347,10 @@ def run_ours(args):
                        "l2": (f"inputs > L2 ({8 * (S + 1) * ncell_local / 1e9:.2f} GB state "
                               f"per GPU)") if 8 * (S + 1) * ncell_local > 126e6 else "fits L2"},
             "chem_rhs_cells_per_s": chem_cells_per_s,
-            "roofline": {"bound": "fp64", "kernel": "chain_kernel (fused fast IVP + chemistry)",
+            "roofline": {"bound": "fp64", "bound_note": "the fp64 pipe: no part of this path is a "
+                                                        "dense contraction (north_star: tensor cores "
+                                                        "are not used); K2 is judged on HBM below",
+                         "kernel": "chain_kernel (fused fast IVP + chemistry)",
                          "achieved": chem_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": chem_tflops / fp64_peak if fp64_peak else None,
                          "traffic": tr.get("chem_chain", {}).get("dram_bytes_per_launch"),
