@@ -140,6 +140,15 @@ int mr_mri_step(mr_ctx* ctx, double t, double H, uint64_t* counters, int* fail_s
 int mr_mri_integrate(mr_ctx* ctx, double t0, double tf, double H, uint64_t* counters,
                      int* fail_stage);
 /* End-to-end variant with HOST buffers: H2D of y_in, the step, D2H of y_out. */
+/* Asynchronous step: enqueued on the context's stream after the work already
+ * queued on `stream` (a cudaStream_t; NULL = the legacy default stream), and
+ * `stream` is made to wait for it; returns without waiting.  The failure key,
+ * the counters (accumulated into `counters`) and the state commit happen in
+ * mr_mri_step_wait, which returns what mr_mri_step would have.  Until then the
+ * context rejects state-touching calls with MR_CONTRACT.  IMEX couplings still
+ * synchronise inside the step (host Newton decisions). */
+int mr_mri_step_async(mr_ctx* ctx, double t, double H, void* stream);
+int mr_mri_step_wait(mr_ctx* ctx, uint64_t* counters, int* fail_stage);
 int mr_mri_step_host(mr_ctx* ctx, double t, double H, const double* y_in, double* y_out,
                      uint64_t* counters, int* fail_stage);
 /* ark_imex_step / ark_imex_integrate (proj/src/mri.cpp:437-557): the

@@ -104,6 +104,8 @@ def lib():
         "mr_state_device_ptr": (C.c_void_p, [vp]),
         "mr_state_dof": (C.c_size_t, [vp]),
         "mr_mri_step": (C.c_int, [vp, C.c_double, C.c_double, _u64p, _ip]),
+        "mr_mri_step_async": (C.c_int, [vp, C.c_double, C.c_double, vp]),
+        "mr_mri_step_wait": (C.c_int, [vp, _u64p, _ip]),
         "mr_mri_integrate": (C.c_int, [vp, C.c_double, C.c_double, C.c_double, _u64p, _ip]),
         "mr_mri_step_host": (C.c_int, [vp, C.c_double, C.c_double, _dp, _dp, _u64p, _ip]),
         "mr_last_failure": (C.c_int, [vp, _ip, _ip, _ip]),
@@ -369,6 +371,19 @@ class Context:
         cnt = self.counters() if counters is None else counters
         stage = C.c_int(-1)
         rc = self.L.mr_mri_step(self.h, t, H, _p(cnt, _u64p), C.byref(stage))
+        self._check(rc, stage.value)
+        return cnt
+
+    def mri_step_async(self, t, H, stream=None):
+        """Enqueue one step after the work queued on `stream` (a cudaStream_t
+        handle as int, or None for the legacy default stream); finish it with
+        mri_step_wait."""
+        self._check(self.L.mr_mri_step_async(self.h, t, H, stream))
+
+    def mri_step_wait(self, counters=None):
+        cnt = self.counters() if counters is None else counters
+        stage = C.c_int(-1)
+        rc = self.L.mr_mri_step_wait(self.h, _p(cnt, _u64p), C.byref(stage))
         self._check(rc, stage.value)
         return cnt
 

@@ -219,6 +219,17 @@ struct mr_ctx {
   double prof_chem = 0, prof_slow = 0, prof_other = 0;
   std::vector<cudaEvent_t> ev_pool;
   int fail_mri = -1, fail_sub = -1, fail_inner = -1;
+  // mr_mri_step_async: everything mr_mri_step_wait needs to finish the step
+  struct Pending {
+    bool active = false;
+    Plan plan;
+    double t = 0.0, H = 0.0;
+    int missing_stage = -1;
+    unsigned long long host_key = 0;
+    std::vector<std::pair<int, size_t>> timed;
+    const double* ycur = nullptr;
+  } pending;
+  cudaEvent_t ev_async_in = nullptr, ev_async_out = nullptr;
 };
 
 namespace {
@@ -932,7 +943,14 @@ int solve_stage(mr_ctx** cs, int n, int i, double t, double H, const Plan& plan,
 
 // One slow step over a domain of slab contexts sharing a device stream (n > 1)
 // or one context (n == 1, possibly an NCCL rank).
-int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int* fail_stage)
+int domain_finish(mr_ctx** cs, int n, const Plan& plan, double t, double H, int missing_stage,
+                  unsigned long long host_key, const std::vector<std::pair<int, size_t>>& timed,
+                  const double* const* ycur, uint64_t* counters, int* fail_stage);
+
+// async: enqueue only (n == 1); the step is finished by domain_finish from
+// mr_mri_step_wait with the state kept in ctx->pending
+int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int* fail_stage,
+                bool async = false)
 {
   mr_ctx* c0 = cs[0];
   if (fail_stage) *fail_stage = -1;
@@ -1054,7 +1072,6 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
   }
 
   // combine failure keys (min over slabs / ranks)
-  unsigned long long key = MR_NO_FAIL;
   if (n == 1 && c0->comm) {
     MR_NCCL_TRY(c0, AllReduce(c0->d_fail, c0->d_fail, 1, ncclUint64, ncclMin, c0->comm, st));
   }
@@ -1062,7 +1079,32 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
     MR_CUDA_TRY(cs[r], cudaMemcpyAsync(cs[r]->h_fail, cs[r]->d_fail, sizeof(unsigned long long),
                                        cudaMemcpyDeviceToHost, st));
   }
-  MR_CUDA_TRY(c0, cudaStreamSynchronize(st));
+  if (async) {
+    mr_ctx::Pending& pd = c0->pending;
+    pd.active = true;
+    pd.plan = plan;
+    pd.t = t;
+    pd.H = H;
+    pd.missing_stage = missing_stage;
+    pd.host_key = host_key;
+    pd.timed = timed;
+    pd.ycur = ycur[0];
+    return MR_OK;
+  }
+  return domain_finish(cs, n, plan, t, H, missing_stage, host_key, timed, ycur.data(), counters,
+                       fail_stage);
+}
+
+// waits for the enqueued step, decodes the failure key, adds the counters and
+// commits the state (domain_step's second half)
+int domain_finish(mr_ctx** cs, int n, const Plan& plan, double t, double H, int missing_stage,
+                  unsigned long long host_key, const std::vector<std::pair<int, size_t>>& timed,
+                  const double* const* ycur, uint64_t* counters, int* fail_stage)
+{
+  mr_ctx* c0 = cs[0];
+  if (fail_stage) *fail_stage = -1;
+  MR_CUDA_TRY(c0, cudaStreamSynchronize(c0->stream));
+  unsigned long long key = MR_NO_FAIL;
   for (int r = 0; r < n; ++r) key = std::min(key, *cs[r]->h_fail);
   key = std::min(key, host_key);
 
@@ -1223,6 +1265,8 @@ void mr_ctx_destroy(mr_ctx* c)
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->comm && nccl_api().ok) nccl_api().CommDestroy(c->comm);
   cudaStreamDestroy(c->stream);
+  if (c->ev_async_in) cudaEventDestroy(c->ev_async_in);
+  if (c->ev_async_out) cudaEventDestroy(c->ev_async_out);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->ev_pack) cudaEventDestroy(c->ev_pack);
   if (c->ev_halo) cudaEventDestroy(c->ev_halo);
@@ -1626,9 +1670,18 @@ int mr_slow_none(mr_ctx* c)
   return MR_OK;
 }
 
+// a context with an asynchronous step in flight accepts only mr_mri_step_wait
+static int pending_guard(mr_ctx* c)
+{
+  if (c && c->pending.active)
+    return set_err(c, MR_CONTRACT, "an asynchronous step is in flight: call mr_mri_step_wait first");
+  return MR_OK;
+}
+
 int mr_state_upload(mr_ctx* c, const double* host)
 {
   if (!c || !host) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   cudaSetDevice(c->device);
   int rc = ensure_state(c);
   if (rc) return rc;
@@ -1642,6 +1695,7 @@ int mr_state_upload(mr_ctx* c, const double* host)
 int mr_state_download(mr_ctx* c, double* host)
 {
   if (!c || !host) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   if (!c->y_state) return set_err(c, MR_CONTRACT, "no state");
   cudaSetDevice(c->device);
   MR_CUDA_TRY(c, cudaMemcpyAsync(host, c->y_state, c->dof * sizeof(double),
@@ -1661,9 +1715,43 @@ size_t mr_state_dof(const mr_ctx* c) { return c ? c->dof : 0; }
 int mr_mri_step(mr_ctx* c, double t, double H, uint64_t* counters, int* fail_stage)
 {
   if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   cudaSetDevice(c->device);
   mr_ctx* cs[1] = {c};
   return domain_step(cs, 1, t, H, counters, fail_stage);
+}
+
+int mr_mri_step_async(mr_ctx* c, double t, double H, void* stream)
+{
+  if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
+  cudaSetDevice(c->device);
+  if (!c->ev_async_in) {
+    MR_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_async_in, cudaEventDisableTiming));
+    MR_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_async_out, cudaEventDisableTiming));
+  }
+  cudaStream_t us = static_cast<cudaStream_t>(stream);
+  MR_CUDA_TRY(c, cudaEventRecord(c->ev_async_in, us));  // after the caller's queued work
+  MR_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_async_in, 0));
+  mr_ctx* cs[1] = {c};
+  int rc = domain_step(cs, 1, t, H, nullptr, nullptr, true);
+  if (rc) return rc;
+  MR_CUDA_TRY(c, cudaEventRecord(c->ev_async_out, c->stream));
+  MR_CUDA_TRY(c, cudaStreamWaitEvent(us, c->ev_async_out, 0));  // caller's later work follows
+  return MR_OK;
+}
+
+int mr_mri_step_wait(mr_ctx* c, uint64_t* counters, int* fail_stage)
+{
+  if (!c) return MR_CONTRACT;
+  if (!c->pending.active) return set_err(c, MR_CONTRACT, "mr_mri_step_wait: no step in flight");
+  cudaSetDevice(c->device);
+  mr_ctx::Pending pd = std::move(c->pending);
+  c->pending = mr_ctx::Pending{};
+  mr_ctx* cs[1] = {c};
+  const double* yc[1] = {pd.ycur};
+  return domain_finish(cs, 1, pd.plan, pd.t, pd.H, pd.missing_stage, pd.host_key, pd.timed, yc,
+                       counters, fail_stage);
 }
 
 // mri_integrate, proj/src/mri.cpp:524-540 (state unchanged on failure)
@@ -1671,6 +1759,7 @@ int mr_mri_integrate(mr_ctx* c, double t0, double tf, double H, uint64_t* counte
                      int* fail_stage)
 {
   if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   if (fail_stage) *fail_stage = -1;
   if (!(tf > t0)) return set_err(c, MR_CONTRACT, "mri_integrate: tf must exceed t0");
   cudaSetDevice(c->device);
@@ -1893,6 +1982,7 @@ int ark_domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, 
 int mr_ark_imex_step(mr_ctx* c, double t, double H, uint64_t* counters, int* fail_stage)
 {
   if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   cudaSetDevice(c->device);
   return ark_domain_step(&c, 1, t, H, counters, fail_stage);
 }
@@ -1934,6 +2024,7 @@ int mr_mri_step_host(mr_ctx* c, double t, double H, const double* y_in, double* 
                      uint64_t* counters, int* fail_stage)
 {
   if (!c || !y_in || !y_out) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   cudaSetDevice(c->device);
   int rc = ensure_state(c);
   if (rc) return rc;

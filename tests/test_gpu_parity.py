@@ -467,3 +467,43 @@ def test_host_buffer_step_failure_keeps_input():
         ctx.mri_step_host(0.0, cfg["H"], bad, y_out)
     assert np.all(y_out == 3.0)
     assert np.array_equal(ctx.download(), bad, equal_nan=True)
+
+
+# ------------------------------------------------------ asynchronous step
+def test_async_step_equals_sync_step():
+    """mr_mri_step_async + mr_mri_step_wait: same state and counters as
+    mr_mri_step, with the step ordered after / before the caller's stream."""
+    import torch
+    a, cfg, y0 = gpu_ctx("C3", 16)
+    b, _, _ = gpu_ctx("C3", 16)
+    H = cfg["H"]
+    c_a = a.mri_step(0.0, H)
+    a.mri_step(H, H, c_a)
+    s = torch.cuda.Stream()
+    c_b = b.counters()
+    b.mri_step_async(0.0, H, s.cuda_stream)
+    with pytest.raises(P.ContractError):  # state-touching calls wait for the step
+        b.download()
+    b.mri_step_wait(c_b)
+    b.mri_step_async(H, H, None)
+    b.mri_step_wait(c_b)
+    assert np.array_equal(c_a, c_b)
+    assert np.array_equal(a.download(), b.download())
+    with pytest.raises(P.ContractError):
+        b.mri_step_wait()
+
+
+def test_async_step_failure_reported_at_wait():
+    ctx, cfg, y0 = gpu_ctx("C3", 16)
+    ref, _, _ = gpu_ctx("C3", 16)
+    bad = y0.copy()
+    bad[9] = np.nan
+    ctx.upload(bad)
+    ref.upload(bad)
+    with pytest.raises(P.IntegrationError) as e_ref:
+        ref.mri_step(0.0, cfg["H"])
+    ctx.mri_step_async(0.0, cfg["H"])
+    with pytest.raises(P.IntegrationError) as e:
+        ctx.mri_step_wait()
+    assert e.value.stage_index == e_ref.value.stage_index
+    assert np.array_equal(ctx.download(), bad, equal_nan=True)  # state unchanged
