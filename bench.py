@@ -202,9 +202,7 @@ def run_ours(args):
         # one-rank NCCL communicator: the multi-GPU rank's code path (pack,
         # grouped send/recv on the comm stream overlapped with the interior
         # stencil, boundary planes, all-reduced failure key) on one GPU
-        os.environ["MR_NCCL_SELF"] = "1"
-        ctx.comm_init(1, 0, P.Context.nccl_unique_id())
-        del os.environ["MR_NCCL_SELF"]
+        ctx.comm_init_loopback()
     t_setup = time.perf_counter()
     cfg, y0 = P.setup_workload(ctx, args.config, n=n, i0=i0, n0_local=n0l, threads=0)
     if cfg.get("d_impl") is not None and dist:

@@ -126,7 +126,8 @@ int mr_newton_config(mr_ctx* ctx, double tolerance, double safety, int max_iters
 /* ---------------- state ---------------- */
 int mr_state_upload(mr_ctx* ctx, const double* host);   /* local slab, species-major */
 int mr_state_download(mr_ctx* ctx, double* host);
-/* device pointer of the current state (valid until the next step) */
+/* device pointer of the current state (valid until the next step; NULL while
+ * an asynchronous step is pending) */
 double* mr_state_device_ptr(mr_ctx* ctx);
 size_t mr_state_dof(const mr_ctx* ctx);
 
@@ -139,16 +140,18 @@ size_t mr_state_dof(const mr_ctx* ctx);
 int mr_mri_step(mr_ctx* ctx, double t, double H, uint64_t* counters, int* fail_stage);
 int mr_mri_integrate(mr_ctx* ctx, double t0, double tf, double H, uint64_t* counters,
                      int* fail_stage);
-/* End-to-end variant with HOST buffers: H2D of y_in, the step, D2H of y_out. */
 /* Asynchronous step: enqueued on the context's stream after the work already
  * queued on `stream` (a cudaStream_t; NULL = the legacy default stream), and
  * `stream` is made to wait for it; returns without waiting.  The failure key,
  * the counters (accumulated into `counters`) and the state commit happen in
  * mr_mri_step_wait, which returns what mr_mri_step would have.  Until then the
  * context rejects state-touching calls with MR_CONTRACT.  IMEX couplings still
- * synchronise inside the step (host Newton decisions). */
+ * synchronise inside the step (host Newton decisions).  The result is
+ * reachable (mr_state_device_ptr, mr_state_download) only after
+ * mr_mri_step_wait: the commit is a host-side buffer swap. */
 int mr_mri_step_async(mr_ctx* ctx, double t, double H, void* stream);
 int mr_mri_step_wait(mr_ctx* ctx, uint64_t* counters, int* fail_stage);
+/* End-to-end variant with HOST buffers: H2D of y_in, the step, D2H of y_out. */
 int mr_mri_step_host(mr_ctx* ctx, double t, double H, const double* y_in, double* y_out,
                      uint64_t* counters, int* fail_stage);
 /* ark_imex_step / ark_imex_integrate (proj/src/mri.cpp:437-557): the
@@ -197,11 +200,14 @@ int mr_all_finite(mr_ctx* ctx, const double* x, size_t n, int* out);
 /* id128: ncclUniqueId bytes from rank 0 (broadcast by the caller).  Call before
  * mr_grid_set; the context then owns the slab [i0, i0 + n0_local) of its rank and
  * exchanges g = order/2 ghost planes per slow evaluation with grouped
- * ncclSend/ncclRecv.  nranks == 1 builds no communicator (periodic single slab)
- * unless the environment sets MR_NCCL_SELF, which builds a one-rank
- * communicator so the NCCL path can be exercised on one GPU. */
+ * ncclSend/ncclRecv.  nranks == 1 builds no communicator (periodic single
+ * slab). */
 int mr_nccl_unique_id(char* id128);
 int mr_comm_init(mr_ctx* ctx, int nranks, int rank, const char* id128);
+/* A one-rank NCCL communicator: the rank's whole NCCL code path (halo
+ * send/recv to itself overlapped with the interior stencil, all-reduced
+ * failure key, all-gathered CG dot products) on one GPU. */
+int mr_comm_init_loopback(mr_ctx* ctx);
 
 /* In-process "virtual ranks" (one GPU, several slab contexts sharing the
  * device): the same slab code path with halos copied device-to-device. */

@@ -119,6 +119,7 @@ def lib():
         "mr_all_finite": (C.c_int, [vp, C.c_void_p, C.c_size_t, _ip]),
         "mr_nccl_unique_id": (C.c_int, [C.c_char_p]),
         "mr_comm_init": (C.c_int, [vp, C.c_int, C.c_int, C.c_char_p]),
+        "mr_comm_init_loopback": (C.c_int, [vp]),
         "mr_group_step": (C.c_int, [C.POINTER(vp), C.c_int, C.c_double, C.c_double, _u64p, _ip]),
         "mr_mechanism_generate": (C.c_int, [C.c_uint64, C.c_int, C.c_int, _dp, _dp, _ip]),
         "mr_initial_condition": (C.c_int, [C.c_uint64, C.c_int, C.c_double, _dp, C.c_int, C.c_int,
@@ -525,6 +526,11 @@ class Context:
     def comm_init(self, nranks, rank, uid: bytes):
         _bind_process_nccl()
         self._check(self.L.mr_comm_init(self.h, nranks, rank, uid))
+
+    def comm_init_loopback(self):
+        """One-rank NCCL communicator: the multi-GPU rank's code path on one GPU."""
+        _bind_process_nccl()
+        self._check(self.L.mr_comm_init_loopback(self.h))
 
 
 def group_step(ctxs, t, H, counters=None):

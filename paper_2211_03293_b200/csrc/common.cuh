@@ -52,17 +52,6 @@ struct ChainArgs {
   unsigned long long* fail;
 };
 
-// Per-cell synthetic Arrhenius chemistry
-struct ChemDev {
-  int S, R, Spad;
-  const double4* rxn;    // {lnA, beta, Ea/Rc, dnu}
-  const int4* rsp;       // {r1, r2, p1, p2}, absent -> S (dummy slot = 1)
-  const double* sp;      // SoA [9][Spad]: h0, a, hb, s0, rhoW, Wrho, c0, c1, c2
-  const int* csr_off;    // [S+1]
-  const int* csr_ent;    // reaction*2 + (product ? 1 : 0), reaction ascending
-  double RuP;            // R_u / P_atm
-};
-
 // Mechanism for the chemistry kernel.  Scalars and per-species data travel
 // in the kernel parameter space (constant bank); the per-reaction records and
 // the production lists live in a device blob that every block stages into
@@ -99,7 +88,6 @@ struct ChemParams {
 
 struct ChemCfg {
   int NW, SPL;  // warps per cell group (slots), components per thread
-  int NG;       // cell groups (of 32 cells) per block, named barriers per group
   bool subdiag;
   int nstage;  // inner table stages (non-subdiagonal tables: stage accumulators)
   int ndeg;
@@ -158,15 +146,14 @@ struct ChainCfg {
   int maxs;  // 4 or 6
   int ndeg;  // 1 or 2
 };
-int chain_pick(ChainCfg* cfg, int fast_kind, int ncomp, int S, int R, int s_f, int ndeg);
-cudaError_t launch_chain(const ChainCfg& cfg, const ChainArgs& a, const ChemDev& ch,
-                         const LinDev& lin, cudaStream_t st);
+int chain_pick(ChainCfg* cfg, int fast_kind, int ncomp, int s_f, int ndeg);
+cudaError_t launch_chain(const ChainCfg& cfg, const ChainArgs& a, const LinDev& lin,
+                         cudaStream_t st);
 cudaError_t launch_fast_rhs(const ChainCfg& cfg, const double* y, double* out, size_t ncell,
-                            int ncomp, const ChemDev& ch, const LinDev& lin, cudaStream_t st);
-size_t chain_smem_bytes(const ChainCfg& cfg, int S, int R, int block);
+                            int ncomp, const LinDev& lin, cudaStream_t st);
 
 int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int ndeg);
-int chem_chunking(int NW, int S, int R, size_t blob_bytes, int* rc, int* nchunk, int NG = 1);
+int chem_chunking(int NW, int S, int R, size_t blob_bytes, int* rc, int* nchunk);
 cudaError_t launch_chem_chain(const ChemCfg& cfg, const ChainArgs& a, const ChemParams& P,
                               cudaStream_t st);
 cudaError_t launch_chem_rhs(const ChemCfg& cfg, const double* y, double* out, size_t ncell,

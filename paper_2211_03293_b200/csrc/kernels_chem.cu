@@ -3,9 +3,6 @@
 // (kernels_chem_nw*.cu).  Kernel design: kernels_chem.cuh.
 #include <cuda_runtime.h>
 
-#include <cstdio>
-#include <cstdlib>
-
 #include "kernels_chem.cuh"
 
 namespace mrchem {
@@ -17,24 +14,15 @@ namespace mrchem {
   extern template cudaError_t run_chem_rhs<A, B>(const double*, double*, size_t, int, const ChemParams&, cudaStream_t);
 MR_DECL(4, 3)
 MR_DECL(8, 3)
-MR_DECL(8, 7)
-MR_DECL(16, 4)
-MR_DECL(24, 3)
 MR_DECL(32, 2)
 #undef MR_DECL
 extern template cudaError_t run_chem_chain<32, 2, false, 3, 1>(const ChainArgs&, const ChemParams&, cudaStream_t);
 extern template cudaError_t run_chem_chain<32, 2, false, 3, 2>(const ChainArgs&, const ChemParams&, cudaStream_t);
-#define MR_DECL_G(A, B, G)                                                                      \
-  extern template cudaError_t run_chem_chain<A, B, true, 4, 1, G>(const ChainArgs&, const ChemParams&, cudaStream_t);  \
-  extern template cudaError_t run_chem_chain<A, B, true, 4, 2, G>(const ChainArgs&, const ChemParams&, cudaStream_t);  \
-  extern template cudaError_t run_chem_chain<A, B, false, 6, 1, G>(const ChainArgs&, const ChemParams&, cudaStream_t); \
-  extern template cudaError_t run_chem_chain<A, B, false, 6, 2, G>(const ChainArgs&, const ChemParams&, cudaStream_t);
-MR_DECL_G(16, 4, 2)
-#undef MR_DECL_G
 }  // namespace mrchem
 
-// (NW warps = slots, SPL components per thread) layouts
-#define MR_CHEM_BLOCK_LAYOUTS(X) X(4, 3) X(8, 3) X(8, 7) X(16, 4) X(24, 3) X(32, 2)
+// (NW warps = slots, SPL components per thread) layouts: C1/C2 (10
+// components), C3 (22), C4/C5 (54); DESIGN.md section 4 for the measurements
+#define MR_CHEM_BLOCK_LAYOUTS(X) X(4, 3) X(8, 3) X(32, 2)
 
 int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int ndeg)
 {
@@ -47,37 +35,22 @@ int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int nd
   cfg->subdiag = subdiag;
   cfg->nstage = tab.s;
   cfg->ndeg = ndeg;
-  cfg->NG = 1;
   if (ncomp <= 12) { cfg->NW = 4; cfg->SPL = 3; }
   else if (ncomp <= 24) { cfg->NW = 8; cfg->SPL = 3; }
   else if (ncomp <= 64) { cfg->NW = 32; cfg->SPL = 2; }
   else return 1;
-  if (const char* env = getenv("MR_CHEM_NG")) {  // experiment hook: two 32-cell groups per block
-    if (atoi(env) == 2 && ncomp <= 64 && ncomp >= 33) { cfg->NW = 16; cfg->SPL = 4; cfg->NG = 2; return 0; }
-  }
-  if (const char* env = getenv("MR_CHEM_BLOCK")) {  // experiment hook "NW,SPL"
-    int nw = 0, spl = 0;
-    if (sscanf(env, "%d,%d", &nw, &spl) == 2 && nw * spl >= ncomp) {
-      bool known = false;
-#define MR_KNOWN(A, B) known |= (nw == A && spl == B);
-      MR_CHEM_BLOCK_LAYOUTS(MR_KNOWN)
-#undef MR_KNOWN
-      if (known) { cfg->NW = nw; cfg->SPL = spl; }
-    }
-  }
   return 0;
 }
 
 // rate-buffer chunking: largest chunk (multiple of NW) such that two blocks
-// fit the 227 KB shared memory of an SM (one block for NW = 16)
-int chem_chunking(int NW, int S, int R, size_t blob_bytes, int* rc, int* nchunk, int NG)
+// fit the 227 KB shared memory of an SM for NW <= 8 (one 1024-thread block
+// for NW = 32)
+int chem_chunking(int NW, int S, int R, size_t blob_bytes, int* rc, int* nchunk)
 {
-  size_t budget = (size_t)(NW <= 8 ? 113 : 227) * 1024;  // 2 blocks/SM for NW <= 8
-  if (NG > 1) budget = 227 * 1024;
-  if (const char* env = getenv("MR_CHEM_BUDGET_KB")) budget = (size_t)atoi(env) * 1024;  // experiment hook
-  const size_t fixed = mrchem::smem_bytes(NW, S + 1, 0, (int)((blob_bytes + 15) / 16), NG);
+  const size_t budget = (size_t)(NW <= 8 ? 113 : 227) * 1024;
+  const size_t fixed = mrchem::smem_bytes(NW, S + 1, 0, (int)((blob_bytes + 15) / 16));
   if (fixed >= budget) return 1;
-  int cap = (int)((budget - fixed) / (256 * (size_t)NG));
+  int cap = (int)((budget - fixed) / 256);
   cap -= cap % NW;
   if (cap < NW) return 1;
   int n = (R + cap - 1) / cap;
@@ -93,24 +66,18 @@ cudaError_t launch_chem_chain(const ChemCfg& cfg, const ChainArgs& a, const Chem
                               cudaStream_t st)
 {
 #define MR_CHEM_DISPATCH(A, B)                                                              \
-  if (cfg.NW == A && cfg.SPL == B && cfg.NG == 1) {                                         \
+  if (cfg.NW == A && cfg.SPL == B) {                                                        \
     if (cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem_chain<A, B, true, 4, 1>(a, P, st);   \
     if (cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem_chain<A, B, true, 4, 2>(a, P, st);   \
     if (!cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem_chain<A, B, false, 6, 1>(a, P, st); \
     if (!cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem_chain<A, B, false, 6, 2>(a, P, st); \
   }
-  if (cfg.NW == 32 && cfg.SPL == 2 && cfg.NG == 1 && !cfg.subdiag && cfg.nstage <= 3) {
+  if (cfg.NW == 32 && cfg.SPL == 2 && !cfg.subdiag && cfg.nstage <= 3) {
     if (cfg.ndeg == 1) return mrchem::run_chem_chain<32, 2, false, 3, 1>(a, P, st);
     if (cfg.ndeg == 2) return mrchem::run_chem_chain<32, 2, false, 3, 2>(a, P, st);
   }
   MR_CHEM_BLOCK_LAYOUTS(MR_CHEM_DISPATCH)
 #undef MR_CHEM_DISPATCH
-  if (cfg.NW == 16 && cfg.SPL == 4 && cfg.NG == 2) {
-    if (cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem_chain<16, 4, true, 4, 1, 2>(a, P, st);
-    if (cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem_chain<16, 4, true, 4, 2, 2>(a, P, st);
-    if (!cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem_chain<16, 4, false, 6, 1, 2>(a, P, st);
-    if (!cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem_chain<16, 4, false, 6, 2, 2>(a, P, st);
-  }
   return cudaErrorInvalidConfiguration;
 }
 

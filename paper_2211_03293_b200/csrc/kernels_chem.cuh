@@ -104,34 +104,10 @@ __device__ __forceinline__ void mr_exp_pair(double x, double& e, double& ei)
 //   tinf double  [3][32]    T, lnT, 1/T
 //   spc  double  [S1][10]   per-species constants {c0,c1 | c2,h0 | a,hb | s0,rhoW | Wrho,-}
 //                            (warp-uniform broadcast LDS.128 instead of indexed LDC)
-__host__ __device__ inline size_t group_bytes(int S1, int rc);
-__host__ __device__ inline size_t smem_bytes(int NW, int S1, int rc, int blob_words, int NG = 1)
+__host__ __device__ inline size_t smem_bytes(int NW, int S1, int rc, int blob_words)
 {
-  if (NG == 1)
-    return (size_t)S1 * 512 + (size_t)S1 * 256 + (size_t)rc * 256 + 256 + (size_t)blob_words * 16 +
-           (size_t)4 * NW * 256 + 3 * 256 + (size_t)S1 * 80;
-  // NG groups: shared blob + species constants, per group CE, D, q, zero row,
-  // tinf; the energy partials alias the group's CE rows (dead between the
-  // last reaction chunk and the species phase)
-  return (size_t)blob_words * 16 + (size_t)S1 * 80 + (size_t)NG * group_bytes(S1, rc);
-}
-
-__host__ __device__ inline size_t group_bytes(int S1, int rc)
-{
-  return (size_t)S1 * 512 + (size_t)S1 * 256 + (size_t)rc * 256 + 256 + 3 * 256;
-}
-
-// block barrier (NG = 1) or the named barrier of cell group g (NG > 1)
-template <int NG>
-__device__ __forceinline__ void grp_sync(int g, int nthreads)
-{
-  if constexpr (NG == 1) {
-    (void)g;
-    (void)nthreads;
-    __syncthreads();
-  } else {
-    asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(nthreads) : "memory");
-  }
+  return (size_t)S1 * 512 + (size_t)S1 * 256 + (size_t)rc * 256 + 256 + (size_t)blob_words * 16 +
+         (size_t)4 * NW * 256 + 3 * 256 + (size_t)S1 * 80;
 }
 
 struct Smem {
@@ -147,39 +123,10 @@ struct Smem {
 
 // carves shared memory and stages the mechanism blob (all threads; ends with
 // a barrier)
-template <int NG = 1>
-__device__ __forceinline__ Smem stage(char* base, const ChemParams& P, int NW, int c, int w, int g = 0)
+__device__ __forceinline__ Smem stage(char* base, const ChemParams& P, int NW, int c, int w)
 {
   const int S1 = P.S + 1;
   Smem m;
-  if constexpr (NG > 1) {
-    uint4* blob = reinterpret_cast<uint4*>(base);
-    double2* spc = reinterpret_cast<double2*>(base + (size_t)P.blob_words * 16);
-    m.rec = reinterpret_cast<const char*>(blob);
-    m.ent = blob + P.ent_base;
-    m.spc = spc;
-    m.CE = base + (size_t)P.blob_words * 16 + (size_t)S1 * 80 + (size_t)g * group_bytes(S1, P.rc);
-    m.D = m.CE + S1 * 512;
-    m.q = m.D + S1 * 256;
-    char* zero = m.q + P.rc * 256;
-    m.tinf = reinterpret_cast<double*>(zero + 256);
-    m.part = reinterpret_cast<double*>(m.CE);
-    for (int i = threadIdx.x; i < P.S; i += blockDim.x) {
-      spc[i * 5 + 0] = make_double2(P.c0[i], P.c1[i]);
-      spc[i * 5 + 1] = make_double2(P.c2[i], P.h0[i]);
-      spc[i * 5 + 2] = make_double2(P.a[i], P.hb[i]);
-      spc[i * 5 + 3] = make_double2(P.s0[i], P.rhoW[i]);
-      spc[i * 5 + 4] = make_double2(P.Wrho[i], 0.0);
-    }
-    for (int i = threadIdx.x; i < P.blob_words; i += blockDim.x) blob[i] = __ldg(P.blob + i);
-    if (w == 0) {
-      reinterpret_cast<double*>(zero)[c] = 0.0;
-      *reinterpret_cast<double2*>(m.CE + P.S * 512 + c * 16) = make_double2(1.0, 1.0);
-      *reinterpret_cast<double*>(m.D + P.S * 256 + c * 8) = 1.0;
-    }
-    __syncthreads();
-    return m;
-  }
   m.CE = base;
   m.D = m.CE + S1 * 512;
   m.q = m.D + S1 * 256;
@@ -239,10 +186,10 @@ __device__ __forceinline__ const T& at(const char* base, unsigned off)
 }
 
 // One chemistry RHS evaluation for the block's 32 cells (all threads call it).
-template <int NW, int SPL, int NG = 1>
+template <int NW, int SPL>
 __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem& m, int w, int c,
                                                 const int (&kk)[SPL], const double (&v)[SPL],
-                                                double (&f)[SPL], int g MR_PH_ARG)
+                                                double (&f)[SPL] MR_PH_ARG)
 {
   MR_PH(0);  // RK bookkeeping since the previous evaluation
   const int S = P.S;
@@ -267,7 +214,7 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
     m.part[(2 * NW + w) * 32 + c] = p2;
     m.part[(3 * NW + w) * 32 + c] = e;
   }
-  grp_sync<NG>(g, NW * 32);
+  __syncthreads();
   MR_PH(1);  // energy partial sums
   if (w == 0) {
     double E0 = 0.0, E1 = 0.0, E2 = 0.0, ee = 0.0;
@@ -284,7 +231,7 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
     m.tinf[1 * 32 + c] = log(T);
     m.tinf[2 * 32 + c] = 1.0 / T;
   }
-  grp_sync<NG>(g, NW * 32);
+  __syncthreads();
   MR_PH(2);  // temperature (warp 0)
   const double T = m.tinf[0 * 32 + c];
   const double lnT = m.tinf[1 * 32 + c];
@@ -316,7 +263,7 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
       }
     }
   }
-  grp_sync<NG>(g, NW * 32);
+  __syncthreads();
   MR_PH(3);  // species rows
 
   double acc[SPL];
@@ -350,7 +297,7 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
       qw += NW * 256;
       rp += NW * (int)sizeof(ChemRec);
     }
-    grp_sync<NG>(g, NW * 32);
+    __syncthreads();
     MR_PH(4);  // reactions (chunk)
     // ---- production: w_k += sum_(producing) q - sum_(consuming) q, reaction
     //      ascending, four entries per broadcast LDS.128 (padding -> zero row).
@@ -379,7 +326,7 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
         acc[t] = s_;
       }
     }
-    if (ch + 1 < P.nchunk) grp_sync<NG>(g, NW * 32);  // q is overwritten by the next chunk
+    if (ch + 1 < P.nchunk) __syncthreads();  // q is overwritten by the next chunk
     MR_PH(5);  // production (warp 0's own lists)
   }
 #pragma unroll
@@ -395,17 +342,16 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
 // 229 -> 196); NW = 32 is one 1024-thread block (64 registers).
 constexpr int chem_min_blocks(int NW, int NDEG)
 {
-  return NW == 4 ? (NDEG == 1 ? 8 : 6) : NW == 8 ? 4 : NW <= 16 ? 2 : 1;
+  return NW == 4 ? (NDEG == 1 ? 8 : 6) : NW == 8 ? 4 : 1;
 }
-template <int NW, int SPL, bool SUBDIAG, int MAXS, int NDEG, int NG = 1>
-__global__ void __launch_bounds__(NW * NG * 32, NG > 1 ? 1 : chem_min_blocks(NW, NDEG))
+template <int NW, int SPL, bool SUBDIAG, int MAXS, int NDEG>
+__global__ void __launch_bounds__(NW * 32, chem_min_blocks(NW, NDEG))
     chem_chain_kernel(const __grid_constant__ ChainArgs a, const __grid_constant__ ChemParams P)
 {
   extern __shared__ __align__(16) double smem_raw[];
   const int c = threadIdx.x & 31;
-  const int g = (int)(threadIdx.x >> 5) / NW;  // cell group (NG > 1: named barriers)
-  const int w = (int)(threadIdx.x >> 5) - g * NW;
-  const size_t cell = ((size_t)blockIdx.x * NG + g) * 32 + c;
+  const int w = (int)(threadIdx.x >> 5);
+  const size_t cell = (size_t)blockIdx.x * 32 + c;
   const bool active = cell < a.ncell;
   const size_t nc = a.ncell;
   const int ncomp = a.ncomp;
@@ -413,7 +359,7 @@ __global__ void __launch_bounds__(NW * NG * 32, NG > 1 ? 1 : chem_min_blocks(NW,
   long long ph_last = clock64();
   const long long ph_begin = ph_last;
 #endif
-  const Smem m = stage<NG>(reinterpret_cast<char*>(smem_raw), P, NW, c, w, g);
+  const Smem m = stage(reinterpret_cast<char*>(smem_raw), P, NW, c, w);
   int kk[SPL];  // components owned by this thread (load-balanced permutation)
 #pragma unroll
   for (int t = 0; t < SPL; ++t) kk[t] = MR_KK(w + NW * t);
@@ -511,7 +457,7 @@ __global__ void __launch_bounds__(NW * NG * 32, NG > 1 ? 1 : chem_min_blocks(NW,
         const double theta = dadd(t0, dmul(a.tab.c[j], h));
         const double tau = __ddiv_rn(dadd(theta, -st.t_start), st.span);
         double f[SPL];
-        chem_block_eval<NW, SPL, NG>(P, m, w, c, kk, stg, f, g MR_PH_PASS);
+        chem_block_eval<NW, SPL>(P, m, w, c, kk, stg, f MR_PH_PASS);
         const double hb = dmul(h, a.tab.b[j]);
         const bool use_b = a.tab.b[j] != 0.0;
         double hA_next = 0.0;
@@ -593,7 +539,7 @@ __global__ void __launch_bounds__(NW * 32) chem_rhs_kernel(const double* __restr
 #ifdef MR_PHASE_PROF
   long long ph_last = clock64();
 #endif
-  chem_block_eval<NW, SPL>(P, m, w, c, kk, v, f, 0 MR_PH_PASS);
+  chem_block_eval<NW, SPL>(P, m, w, c, kk, v, f MR_PH_PASS);
 #pragma unroll
   for (int t = 0; t < SPL; ++t) {
     const int k = kk[t];
@@ -601,15 +547,15 @@ __global__ void __launch_bounds__(NW * 32) chem_rhs_kernel(const double* __restr
   }
 }
 
-template <int NW, int SPL, bool SUBDIAG, int MAXS, int NDEG, int NG = 1>
+template <int NW, int SPL, bool SUBDIAG, int MAXS, int NDEG>
 cudaError_t run_chem_chain(const ChainArgs& a, const ChemParams& P, cudaStream_t st)
 {
-  const size_t smem = smem_bytes(NW, P.S + 1, P.rc, P.blob_words, NG);
-  auto k = chem_chain_kernel<NW, SPL, SUBDIAG, MAXS, NDEG, NG>;
+  const size_t smem = smem_bytes(NW, P.S + 1, P.rc, P.blob_words);
+  auto k = chem_chain_kernel<NW, SPL, SUBDIAG, MAXS, NDEG>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const size_t blocks = (a.ncell + 32 * NG - 1) / (32 * NG);
-  k<<<(unsigned)blocks, NW * NG * 32, smem, st>>>(a, P);
+  const size_t blocks = (a.ncell + 31) / 32;
+  k<<<(unsigned)blocks, NW * 32, smem, st>>>(a, P);
   return cudaGetLastError();
 }
 

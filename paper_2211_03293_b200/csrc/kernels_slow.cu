@@ -957,14 +957,12 @@ __global__ void fp64_peak_kernel(double* sink, int iters)
 
 bool stencil_plane_ranges(const StencilArgs& a)
 {
-  static const bool v2 = getenv("MR_STENCIL_V1") == nullptr;  // A/B hook
-  return v2 && a.M == 4 && a.n1 % kV3TJ == 0 && a.n2 % kV2TK == 0;
+  return a.M == 4 && a.n1 % kV3TJ == 0 && a.n2 % kV2TK == 0;
 }
 
 cudaError_t launch_stencil(const StencilArgs& a, cudaStream_t st)
 {
   const size_t ncell = (size_t)a.n0l * a.n1 * a.n2;
-  static const bool v2 = getenv("MR_STENCIL_V1") == nullptr;  // A/B hook
   const bool full = a.i_lo == 0 && a.i_hi == a.n0l;
   if (!full && !stencil_plane_ranges(a)) return cudaErrorInvalidValue;
   if (a.i_hi <= a.i_lo) return cudaSuccess;
@@ -1004,7 +1002,7 @@ cudaError_t launch_stencil(const StencilArgs& a, cudaStream_t st)
     }
     return cudaGetLastError();
   }
-  if (v2 && a.n1 % kV2TJ == 0 && a.n2 % kV2TK == 0) {
+  if (a.n1 % kV2TJ == 0 && a.n2 % kV2TK == 0) {
     const size_t tiles = (size_t)(a.n1 / kV2TJ) * (a.n2 / kV2TK) * a.ncomp;
     int iper = a.n0l;
     while (iper > 16 && tiles * ((a.n0l + iper - 1) / iper) < 148 * 8) iper = (iper + 1) / 2;
@@ -1488,8 +1486,7 @@ cudaError_t launch_lap7(int mode, const LapArgs& a, const double* y, const doubl
                         const double* hi, const double* known, const double* w, double* o1,
                         double* o2, double* o3, double* part, double* part2, cudaStream_t st)
 {
-  static const bool tiled = getenv("MR_LAP7_ROWS") == nullptr;  // A/B hook
-  if (tiled && a.n1 % kLTJ == 0 && a.n2 % kLTK == 0) {
+  if (a.n1 % kLTJ == 0 && a.n2 % kLTK == 0) {
     const size_t sm = lap7_tile_smem();
     if (mode == 0) {
       cudaFuncSetAttribute(lap7_tile_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

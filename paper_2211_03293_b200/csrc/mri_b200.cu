@@ -168,7 +168,6 @@ struct mr_ctx {
   int fast_kind = -1, slow_kind = -1;
   int S = 0, R = 0;
   double rho = 0.0;
-  ChemDev chem{};
   ChemParams* chemP = nullptr;  // host copy, passed by value to the kernels
   double chem_flops = 0.0;
   std::vector<void*> chem_bufs;
@@ -203,6 +202,7 @@ struct mr_ctx {
   double *send_lo = nullptr, *send_hi = nullptr, *recv_lo = nullptr, *recv_hi = nullptr;
   size_t halo_elems = 0;
   double *scr_in = nullptr, *scr_out = nullptr;
+  double* y_backup = nullptr;  // state at the start of an integrate call (restored on failure)
   unsigned long long* d_fail = nullptr;
   unsigned long long* h_fail = nullptr;
   double* d_red = nullptr;  // partials + out
@@ -281,6 +281,7 @@ void free_state(mr_ctx* c)
   free_dev_t(c->recv_hi);
   free_dev_t(c->scr_in);
   free_dev_t(c->scr_out);
+  free_dev_t(c->y_backup);
   free_dev_t(c->cg_known);
   free_dev_t(c->cg_r);
   free_dev_t(c->cg_z);
@@ -990,7 +991,7 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
   if (c0->fast_kind == FK_CHEM) {
     if (chem_pick(&ccfg, c0->ncomp, c0->S, c0->R, c0->tab, ndeg_of(c0)))
       return set_err(c0, MR_CONTRACT, "unsupported mechanism size / table for the chemistry kernel");
-  } else if (chain_pick(&cfg, c0->fast_kind, c0->ncomp, c0->S, c0->R, c0->tab.s, ndeg_of(c0))) {
+  } else if (chain_pick(&cfg, c0->fast_kind, c0->ncomp, c0->tab.s, ndeg_of(c0))) {
     return set_err(c0, MR_CONTRACT, "unsupported component count / table for the fused IVP kernel");
   }
   for (int r = 0; r < n; ++r)
@@ -1063,7 +1064,7 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
         if (c->fast_kind == FK_CHEM)
           MR_CUDA_TRY(c, launch_chem_chain(ccfg, a, *c->chemP, st));
         else
-          MR_CUDA_TRY(c, launch_chain(cfg, a, c->chem, c->fastA, st));
+          MR_CUDA_TRY(c, launch_chain(cfg, a, c->fastA, st));
         c->launches++;
         ycur[r] = c->y_work;
       }
@@ -1216,6 +1217,16 @@ int read_coupling_text(const char* text, Coupling& cp, std::string& err)
 
 }  // namespace
 
+// a context with an asynchronous step in flight accepts only mr_mri_step_wait
+// (and the read-only queries): every entry point that touches the state, the
+// buffers or the configuration calls this first
+static int pending_guard(mr_ctx* c)
+{
+  if (c && c->pending.active)
+    return set_err(c, MR_CONTRACT, "an asynchronous step is in flight: call mr_mri_step_wait first");
+  return MR_OK;
+}
+
 // ===========================================================================
 // C-ABI
 // ===========================================================================
@@ -1278,6 +1289,7 @@ const char* mr_last_error(const mr_ctx* c) { return c ? c->err.c_str() : "null c
 int mr_grid_set(mr_ctx* c, int n0, int n1, int n2, int n_comp, double length, int i0, int n0_local)
 {
   if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   if (n0 < 1 || n1 < 1 || n2 < 1 || n_comp < 1 || !(length > 0.0) || i0 < 0 || n0_local < 1 ||
       i0 + n0_local > n0)
     return set_err(c, MR_CONTRACT, "mr_grid_set: bad grid");
@@ -1295,6 +1307,7 @@ int mr_grid_set(mr_ctx* c, int n0, int n1, int n2, int n_comp, double length, in
 int mr_coupling_load(mr_ctx* c, int s, int n_deg, const double* cc, const int* kind,
                      const double* gamma, const double* omega)
 {
+  if (int g = pending_guard(c)) return g;
   if (!c || !cc || !kind || s < 2 || s > kMaxStages || n_deg < 1 || n_deg > 8)
     return set_err(c, MR_CONTRACT, "mr_coupling_load: bad arguments");
   Coupling cp;
@@ -1320,6 +1333,7 @@ int mr_coupling_load(mr_ctx* c, int s, int n_deg, const double* cc, const int* k
 int mr_coupling_load_text(mr_ctx* c, const char* text)
 {
   if (!c || !text) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   Coupling cp;
   std::string err;
   int rc = read_coupling_text(text, cp, err);
@@ -1333,6 +1347,7 @@ int mr_coupling_load_text(mr_ctx* c, const char* text)
 
 int mr_table_load(mr_ctx* c, int s, const double* A, const double* b, const double* cc)
 {
+  if (int g = pending_guard(c)) return g;
   if (!c || !A || !b || !cc || s < 1 || s > MR_MAXS)
     return set_err(c, MR_CONTRACT, "mr_table_load: bad arguments");
   TableDev t{};
@@ -1353,6 +1368,7 @@ int mr_table_load(mr_ctx* c, int s, const double* A, const double* b, const doub
 
 int mr_set_substeps(mr_ctx* c, int m)
 {
+  if (int g = pending_guard(c)) return g;
   if (!c || m < 1) return set_err(c, MR_CONTRACT, "m must be >= 1");
   c->m = m;
   return MR_OK;
@@ -1361,6 +1377,7 @@ int mr_set_substeps(mr_ctx* c, int m)
 int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species,
                       const double* reactions, const int* rspecies)
 {
+  if (int g = pending_guard(c)) return g;
   if (!c || S < 1 || R < 1 || !(rho > 0.0) || !species || !reactions || !rspecies)
     return set_err(c, MR_CONTRACT, "mr_fast_chemistry: bad arguments");
   cudaSetDevice(c->device);
@@ -1414,18 +1431,6 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
     c->chem_bufs.push_back(d);
     return d;
   };
-  ChemDev ch{};
-  ch.S = S;
-  ch.R = R;
-  ch.Spad = Sp;
-  ch.sp = (const double*)up(sp.data(), sp.size() * sizeof(double));
-  ch.rxn = (const double4*)up(rx.data(), rx.size() * sizeof(double4));
-  ch.rsp = (const int4*)up(rs.data(), rs.size() * sizeof(int4));
-  ch.csr_off = (const int*)up(cnt.data(), cnt.size() * sizeof(int));
-  ch.csr_ent = (const int*)up(ent.data(), ent.size() * sizeof(int));
-  ch.RuP = kRu / kPatm;
-  if (!ch.sp || !ch.rxn || !ch.rsp || !ch.csr_off || !ch.csr_ent)
-    return set_err(c, MR_CUDA, "mr_fast_chemistry: device allocation failed");
   // chemistry kernel parameters: per-species data in the constant bank,
   // reaction records + production lists in a blob staged into shared memory
   if (S + 1 > MR_CHEM_MAXS || R > MR_CHEM_MAXR)
@@ -1460,7 +1465,7 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
                               4 * ((size_t)nnz + 2 * 3 * (size_t)S * MR_CHEM_MAXCHUNK) + 16;
     int rcz = 0, nch = 0;
     if (chem_pick(&lay, S + 1, S, R, t4, 1) ||
-        chem_chunking(lay.NW, S, R, blob_bound, &rcz, &nch, lay.NG))
+        chem_chunking(lay.NW, S, R, blob_bound, &rcz, &nch))
       return set_err(c, MR_CONTRACT, "mechanism too large for the chemistry kernel's shared memory");
     P.rc = rcz;
     P.nchunk = nch;
@@ -1474,11 +1479,6 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
       std::vector<double> load(NW, 0.0);
       std::vector<int> used(NW, 0);
       for (int i = 0; i < MR_CHEM_MAXS; ++i) P.perm[i] = 255;
-      const bool identity = getenv("MR_CHEM_NOPERM") != nullptr;  // experiment hook
-      if (identity) {
-        for (int i = 0; i < NW * SPL && i <= S; ++i) P.perm[i] = (unsigned char)i;
-        order.clear();
-      }
       for (int k : order) {
         int best = -1;
         for (int w2 = 0; w2 < NW; ++w2)
@@ -1529,7 +1529,6 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
     P.blob_words = (int)(blob_bytes / 16);
     P.ent_base = (int)(rec_bytes / 16);
   }
-  c->chem = ch;
   c->S = S;
   c->R = R;
   c->rho = rho;
@@ -1553,6 +1552,7 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
 
 int mr_fast_linear(mr_ctx* c, const double* A)
 {
+  if (int g = pending_guard(c)) return g;
   if (!c || !A || !c->has_grid || c->ncomp > MR_MAXLIN)
     return set_err(c, MR_CONTRACT, "mr_fast_linear: needs grid with n_comp <= 8");
   c->fastA.n = c->ncomp;
@@ -1564,6 +1564,7 @@ int mr_fast_linear(mr_ctx* c, const double* A)
 int mr_fast_none(mr_ctx* c)
 {
   if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   c->fast_kind = FK_NONE;
   return MR_OK;
 }
@@ -1571,6 +1572,7 @@ int mr_fast_none(mr_ctx* c)
 int mr_slow_stencil(mr_ctx* c, int order, double diffusion, const double* u, const double* prof,
                     int nmax)
 {
+  if (int g = pending_guard(c)) return g;
   if (!c || !c->has_grid || (order != 2 && order != 4 && order != 8) || diffusion < 0.0)
     return set_err(c, MR_CONTRACT, "mr_slow_stencil: bad arguments (order 2/4/8, grid first)");
   cudaSetDevice(c->device);
@@ -1604,6 +1606,7 @@ static int ensure_scratch(mr_ctx* c);
 
 int mr_slow_implicit_diffusion(mr_ctx* c, double d_impl, int cg_iters)
 {
+  if (int g = pending_guard(c)) return g;
   if (!c || c->slow_kind != SK_STENCIL || !(d_impl >= 0.0) || cg_iters < 0)
     return set_err(c, MR_CONTRACT,
                    "mr_slow_implicit_diffusion: needs the stencil plugin, d_impl >= 0, cg_iters >= 0");
@@ -1616,6 +1619,7 @@ int mr_slow_implicit_diffusion(mr_ctx* c, double d_impl, int cg_iters)
 int mr_newton_config(mr_ctx* c, double tolerance, double safety, int max_iters,
                      const double* weights)
 {
+  if (int g = pending_guard(c)) return g;
   if (!c || !(tolerance > 0.0) || !(safety > 0.0) || safety > 1.0 || max_iters < 0)
     return set_err(c, MR_CONTRACT, "newton_solve: bad NewtonConfig");
   if (weights && !c->has_grid) return set_err(c, MR_CONTRACT, "grid not set (mr_grid_set)");
@@ -1635,6 +1639,7 @@ int mr_implicit_rhs(mr_ctx* c, double t, const double* y, double* out)
 {
   (void)t;
   if (!c || !y || !out) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   if (!c->imex) return set_err(c, MR_CONTRACT, "mr_implicit_rhs: no implicit partition configured");
   cudaSetDevice(c->device);
   int rc = ensure_scratch(c);
@@ -1653,6 +1658,7 @@ int mr_implicit_rhs(mr_ctx* c, double t, const double* y, double* out)
 
 int mr_slow_linear(mr_ctx* c, const double* A)
 {
+  if (int g = pending_guard(c)) return g;
   if (!c || !A || !c->has_grid || c->ncomp > MR_MAXLIN)
     return set_err(c, MR_CONTRACT, "mr_slow_linear: needs grid with n_comp <= 8");
   c->imex = false;
@@ -1665,16 +1671,9 @@ int mr_slow_linear(mr_ctx* c, const double* A)
 int mr_slow_none(mr_ctx* c)
 {
   if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   c->slow_kind = SK_NONE;
   c->imex = false;
-  return MR_OK;
-}
-
-// a context with an asynchronous step in flight accepts only mr_mri_step_wait
-static int pending_guard(mr_ctx* c)
-{
-  if (c && c->pending.active)
-    return set_err(c, MR_CONTRACT, "an asynchronous step is in flight: call mr_mri_step_wait first");
   return MR_OK;
 }
 
@@ -1704,9 +1703,11 @@ int mr_state_download(mr_ctx* c, double* host)
   return MR_OK;
 }
 
+// the result of an asynchronous step becomes the state at mr_mri_step_wait
+// (the commit is a host-side buffer swap): no pointer while one is pending
 double* mr_state_device_ptr(mr_ctx* c)
 {
-  if (!c || ensure_state(c)) return nullptr;
+  if (!c || pending_guard(c) || ensure_state(c)) return nullptr;
   return c->y_state;
 }
 
@@ -1734,10 +1735,21 @@ int mr_mri_step_async(mr_ctx* c, double t, double H, void* stream)
   MR_CUDA_TRY(c, cudaEventRecord(c->ev_async_in, us));  // after the caller's queued work
   MR_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_async_in, 0));
   mr_ctx* cs[1] = {c};
-  int rc = domain_step(cs, 1, t, H, nullptr, nullptr, true);
-  if (rc) return rc;
-  MR_CUDA_TRY(c, cudaEventRecord(c->ev_async_out, c->stream));
-  MR_CUDA_TRY(c, cudaStreamWaitEvent(us, c->ev_async_out, 0));  // caller's later work follows
+  const int rc = domain_step(cs, 1, t, H, nullptr, nullptr, true);
+  // the caller's stream follows whatever was enqueued, also when the enqueue
+  // failed part-way (kernels already queued keep reading the state)
+  const cudaError_t e1 = cudaEventRecord(c->ev_async_out, c->stream);
+  const cudaError_t e2 = cudaStreamWaitEvent(us, c->ev_async_out, 0);
+  if (rc) {
+    cudaStreamSynchronize(c->stream);
+    c->pending = mr_ctx::Pending{};
+    return rc;
+  }
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    c->pending = mr_ctx::Pending{};
+    return set_err(c, MR_CUDA, std::string("mr_mri_step_async: ") +
+                                   cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+  }
   return MR_OK;
 }
 
@@ -1767,8 +1779,9 @@ int mr_mri_integrate(mr_ctx* c, double t0, double tf, double H, uint64_t* counte
   if (rc) return rc;
   const long n_steps = static_cast<long>(std::ceil((tf - t0) / H - 1e-12));
   double* backup = nullptr;
-  if (n_steps > 1) {
-    MR_CUDA_TRY(c, cudaMalloc(&backup, c->dof * sizeof(double)));
+  if (n_steps > 1) {  // allocated once per grid, reused by every integrate call
+    if (!c->y_backup) MR_CUDA_TRY(c, cudaMalloc(&c->y_backup, c->dof * sizeof(double)));
+    backup = c->y_backup;
     MR_CUDA_TRY(c, cudaMemcpyAsync(backup, c->y_state, c->dof * sizeof(double),
                                    cudaMemcpyDeviceToDevice, c->stream));
   }
@@ -1784,7 +1797,6 @@ int mr_mri_integrate(mr_ctx* c, double t0, double tf, double H, uint64_t* counte
       cudaMemcpyAsync(c->y_state, backup, c->dof * sizeof(double), cudaMemcpyDeviceToDevice,
                       c->stream);
     cudaStreamSynchronize(c->stream);
-    cudaFree(backup);
   }
   return rc;
 }
@@ -1991,6 +2003,7 @@ int mr_ark_imex_integrate(mr_ctx* c, double t0, double tf, double H, uint64_t* c
                           int* fail_stage)
 {
   if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   if (fail_stage) *fail_stage = -1;
   if (!(tf > t0)) return set_err(c, MR_CONTRACT, "ark_imex_integrate: tf must exceed t0");
   cudaSetDevice(c->device);
@@ -1998,8 +2011,9 @@ int mr_ark_imex_integrate(mr_ctx* c, double t0, double tf, double H, uint64_t* c
   if (rc) return rc;
   const long n_steps = static_cast<long>(std::ceil((tf - t0) / H - 1e-12));
   double* backup = nullptr;
-  if (n_steps > 1) {
-    MR_CUDA_TRY(c, cudaMalloc(&backup, c->dof * sizeof(double)));
+  if (n_steps > 1) {  // allocated once per grid, reused by every integrate call
+    if (!c->y_backup) MR_CUDA_TRY(c, cudaMalloc(&c->y_backup, c->dof * sizeof(double)));
+    backup = c->y_backup;
     MR_CUDA_TRY(c, cudaMemcpyAsync(backup, c->y_state, c->dof * sizeof(double),
                                    cudaMemcpyDeviceToDevice, c->stream));
   }
@@ -2015,7 +2029,6 @@ int mr_ark_imex_integrate(mr_ctx* c, double t0, double tf, double H, uint64_t* c
       cudaMemcpyAsync(c->y_state, backup, c->dof * sizeof(double), cudaMemcpyDeviceToDevice,
                       c->stream);
     cudaStreamSynchronize(c->stream);
-    cudaFree(backup);
   }
   return rc;
 }
@@ -2058,6 +2071,7 @@ int mr_fast_rhs(mr_ctx* c, double t, const double* y, double* out)
 {
   (void)t;
   if (!c || !y || !out) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   if (!c->has_grid || c->fast_kind < 0) return set_err(c, MR_CONTRACT, "fast plugin not set");
   if (c->fast_kind == FK_CHEM && c->ncomp != c->S + 1)
     return set_err(c, MR_CONTRACT, "chemistry plugin needs n_comp == S + 1");
@@ -2076,10 +2090,10 @@ int mr_fast_rhs(mr_ctx* c, double t, const double* y, double* out)
                                    c->stream));
   } else {
     ChainCfg cfg;
-    if (chain_pick(&cfg, c->fast_kind, c->ncomp, c->S, c->R, 4, 1))
+    if (chain_pick(&cfg, c->fast_kind, c->ncomp, 4, 1))
       return set_err(c, MR_CONTRACT, "unsupported component count");
-    MR_CUDA_TRY(c, launch_fast_rhs(cfg, c->scr_in, c->scr_out, c->ncell, c->ncomp, c->chem,
-                                   c->fastA, c->stream));
+    MR_CUDA_TRY(c, launch_fast_rhs(cfg, c->scr_in, c->scr_out, c->ncell, c->ncomp, c->fastA,
+                                   c->stream));
   }
   c->launches++;
   MR_CUDA_TRY(c, cudaMemcpyAsync(out, c->scr_out, c->dof * sizeof(double), cudaMemcpyDeviceToHost,
@@ -2100,9 +2114,9 @@ static int eval_fast_dev(mr_ctx* c, const double* in, double* out)
     MR_CUDA_TRY(c, launch_chem_rhs(ccfg, in, out, c->ncell, c->ncomp, *c->chemP, c->stream));
   } else {
     ChainCfg cfg;
-    if (chain_pick(&cfg, c->fast_kind, c->ncomp, c->S, c->R, 4, 1))
+    if (chain_pick(&cfg, c->fast_kind, c->ncomp, 4, 1))
       return set_err(c, MR_CONTRACT, "unsupported component count");
-    MR_CUDA_TRY(c, launch_fast_rhs(cfg, in, out, c->ncell, c->ncomp, c->chem, c->fastA, c->stream));
+    MR_CUDA_TRY(c, launch_fast_rhs(cfg, in, out, c->ncell, c->ncomp, c->fastA, c->stream));
   }
   c->launches++;
   return MR_OK;
@@ -2227,6 +2241,7 @@ int mr_erk_integrate(mr_ctx* c, int s, const double* A, const double* b, const d
 {
   (void)cvec;  // sum_rhs of the plugins is autonomous: t + c_i h is not consumed
   if (!c || !A || !b) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   return erk_integrate_dev(c, s, A, b, t0, tf, h, n_explicit_evals, fail_stage);
 }
 
@@ -2234,6 +2249,8 @@ int mr_erk_integrate(mr_ctx* c, int s, const double* A, const double* b, const d
 // (butcher.cpp:305-321, written exactly as there), no counters.
 int mr_reference_solution(mr_ctx* c, double t0, double tf, double h, int* fail_stage)
 {
+  if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   double A[6][6] = {{0}}, b[6] = {0};
   A[1][0] = 1.0 / 5.0;
   A[2][0] = 3.0 / 40.0; A[2][1] = 9.0 / 40.0;
@@ -2249,6 +2266,7 @@ int mr_slow_rhs(mr_ctx* c, double t, const double* y, double* out)
 {
   (void)t;
   if (!c || !y || !out) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   if (!c->has_grid || c->slow_kind < 0) return set_err(c, MR_CONTRACT, "slow plugin not set");
   if (c->slow_kind == SK_STENCIL && c->n0l < c->M)
     return set_err(c, MR_CONTRACT, "slab thinner than the stencil ghost width");
@@ -2276,6 +2294,7 @@ int mr_slow_rhs(mr_ctx* c, double t, const double* y, double* out)
 static int reduce(mr_ctx* c, int kind, const double* x, const double* w, size_t n, double* out)
 {
   if (!c || !x || !out) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   cudaSetDevice(c->device);
   const int nb = reduce_blocks();
   double* part = c->d_red;
@@ -2343,19 +2362,8 @@ int mr_nccl_unique_id(char* id128)
   return MR_OK;
 }
 
-int mr_comm_init(mr_ctx* c, int nranks, int rank, const char* id128)
+static int comm_init_nccl(mr_ctx* c, int nranks, int rank, const char* id128)
 {
-  if (!c || nranks < 1 || rank < 0 || rank >= nranks || !id128) return MR_CONTRACT;
-  cudaSetDevice(c->device);
-  // nranks == 1: no communicator, the periodic single-slab path -- unless
-  // MR_NCCL_SELF is set, which builds a one-rank NCCL communicator so the whole
-  // NCCL path (halo send/recv to itself, failure-key all-reduce, all-gathered
-  // CG dot products) runs on one GPU (tests compare it with the plain path)
-  if (nranks == 1 && !getenv("MR_NCCL_SELF")) {
-    c->nranks = 1;
-    c->rank = 0;
-    return MR_OK;
-  }
   ncclUniqueId id;
   std::memcpy(id.internal, id128, NCCL_UNIQUE_ID_BYTES);
   MR_NCCL_TRY(c, CommInitRank(&c->comm, nranks, id, rank));
@@ -2365,12 +2373,44 @@ int mr_comm_init(mr_ctx* c, int nranks, int rank, const char* id128)
   return MR_OK;
 }
 
+int mr_comm_init(mr_ctx* c, int nranks, int rank, const char* id128)
+{
+  if (!c || nranks < 1 || rank < 0 || rank >= nranks || !id128) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
+  if (c->comm) return set_err(c, MR_CONTRACT, "mr_comm_init: communicator already set");
+  cudaSetDevice(c->device);
+  if (nranks == 1) {  // no communicator: the periodic single-slab path
+    c->nranks = 1;
+    c->rank = 0;
+    return MR_OK;
+  }
+  return comm_init_nccl(c, nranks, rank, id128);
+}
+
+// one-rank NCCL communicator: the whole NCCL path (halo send/recv to itself,
+// failure-key all-reduce, all-gathered CG dot products) on one GPU, so tests
+// and the benchmark can compare it with the plain single-slab path
+int mr_comm_init_loopback(mr_ctx* c)
+{
+  if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
+  if (c->comm) return set_err(c, MR_CONTRACT, "mr_comm_init_loopback: communicator already set");
+  cudaSetDevice(c->device);
+  ncclUniqueId id;
+  if (!nccl_api().ok) return set_err(c, MR_CUDA, "NCCL (libnccl.so.2) not available");
+  if (nccl_api().GetUniqueId(&id) != ncclSuccess) return set_err(c, MR_CUDA, "ncclGetUniqueId failed");
+  return comm_init_nccl(c, 1, 0, reinterpret_cast<const char*>(id.internal));
+}
+
 int mr_group_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int* fail_stage)
 {
   if (!cs || n < 1) return MR_CONTRACT;
-  for (int r = 0; r < n; ++r)
+  for (int r = 0; r < n; ++r) {
     if (!cs[r] || cs[r]->device != cs[0]->device || cs[r]->nranks != 1 || cs[r]->comm)
       return set_err(cs[0], MR_CONTRACT, "mr_group_step: contexts must share one device");
+    if (cs[r]->pending.active)
+      return set_err(cs[0], MR_CONTRACT, "an asynchronous step is in flight: call mr_mri_step_wait first");
+  }
   cudaSetDevice(cs[0]->device);
   // order all slabs on the first context's stream
   for (int r = 1; r < n; ++r) cudaStreamSynchronize(cs[r]->stream);
@@ -2543,6 +2583,7 @@ int mr_fp64_peak(mr_ctx* c, double* tflops)
 int mr_set_profiling(mr_ctx* c, int enable)
 {
   if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
   c->profile = enable != 0;
   return MR_OK;
 }

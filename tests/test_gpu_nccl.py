@@ -1,5 +1,5 @@
 """The NCCL path of the slab decomposition on one GPU: a one-rank NCCL
-communicator (MR_NCCL_SELF) sends the halo planes to itself with grouped
+communicator (mr_comm_init_loopback) sends the halo planes to itself with grouped
 ncclSend/ncclRecv, all-reduces the failure key and all-gathers the CG dot
 products -- every collective the multi-GPU run issues.  Its
 results must equal the plain single-slab path bit for bit (same data, same
@@ -17,9 +17,7 @@ def _pair(monkeypatch, name, n, cfg):
     plain = P.Context(0)
     P.setup_workload(plain, name, n=n, config=cfg)
     nccl = P.Context(0)
-    monkeypatch.setenv("MR_NCCL_SELF", "1")
-    nccl.comm_init(1, 0, P.Context.nccl_unique_id())
-    monkeypatch.delenv("MR_NCCL_SELF")
+    nccl.comm_init_loopback()
     cfg_, y0 = P.setup_workload(nccl, name, n=n, config=cfg)
     return plain, nccl, cfg_, y0
 

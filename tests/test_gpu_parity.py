@@ -507,3 +507,78 @@ def test_async_step_failure_reported_at_wait():
         ctx.mri_step_wait()
     assert e.value.stage_index == e_ref.value.stage_index
     assert np.array_equal(ctx.download(), bad, equal_nan=True)  # state unchanged
+
+
+def test_async_step_rejects_state_and_config_calls():
+    """While a step is in flight every entry point that touches the state,
+    the buffers or the configuration raises ContractError (the pending step
+    still reads them); after the wait the result equals the synchronous step."""
+    a, cfg, y0 = gpu_ctx("C3", 16)
+    ref, _, _ = gpu_ctx("C3", 16)
+    H = cfg["H"]
+    c_ref = ref.mri_step(0.0, H)
+    a.mri_step_async(0.0, H)
+    sp, rx, rs = cfg["mech"]
+    calls = [
+        lambda: a.reference_solution(0.0, H, H),
+        lambda: a.ark_imex_integrate(0.0, H, H),
+        lambda: a.erk_integrate("classic-rk4", 0.0, H, H),
+        lambda: a.grid(16, 16, 16, cfg["S"] + 1),
+        lambda: a.load_coupling("mis-kw3"),
+        lambda: a.load_table("classic-rk4"),
+        lambda: a.fast_chemistry(cfg["S"], cfg["R"], cfg["rho"], sp, rx, rs),
+        lambda: a.slow_stencil(8, 0.0),
+        lambda: a.newton_config(),
+        lambda: a.upload(y0),
+        lambda: a.download(),
+        lambda: a.fast_rhs(y0),
+        lambda: a.slow_rhs(y0),
+        lambda: a.mri_step(0.0, H),
+        lambda: a.mri_integrate(0.0, 2 * H, H),
+        lambda: a.mri_step_async(0.0, H),
+        lambda: P.group_step([a], 0.0, H),
+        lambda: a.set_profiling(True),
+    ]
+    for f in calls:
+        with pytest.raises(P.ContractError):
+            f()
+    assert not a.state_ptr()  # the result is reachable only after the wait
+    c = a.mri_step_wait()
+    assert np.array_equal(c, c_ref)
+    assert np.array_equal(a.download(), ref.download())
+
+
+def _device_view(ptr, n):
+    """torch view of n doubles at a raw device pointer (no copy)."""
+    import torch
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_Arr(), device="cuda")
+
+
+def test_async_step_is_ordered_on_the_callers_stream():
+    """The step starts after the work already queued on the caller's stream
+    (a delayed copy of the initial state into the state buffer) and the
+    caller's later work (an overwrite of the input buffer) runs after it."""
+    import torch
+    a, cfg, y0 = gpu_ctx("C3", 16)
+    ref, _, _ = gpu_ctx("C3", 16)
+    H = cfg["H"]
+    c_ref = ref.mri_step(0.0, H)
+    a.upload(np.zeros_like(y0))  # garbage until the caller's copy lands
+    src = torch.from_numpy(y0).cuda()
+    torch.cuda.synchronize()
+    state = _device_view(a.state_ptr(), y0.size)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(50_000_000)  # the copy lands late
+        state.copy_(src)
+    a.mri_step_async(0.0, H, s.cuda_stream)
+    with torch.cuda.stream(s):  # queued after the step: must not disturb it
+        state.zero_()
+    c = a.mri_step_wait()
+    s.synchronize()
+    assert np.array_equal(c, c_ref)
+    assert np.array_equal(a.download(), ref.download())
