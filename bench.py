@@ -85,17 +85,20 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def ncu_traffic():
+def ncu_traffic(n):
     """DRAM bytes per launch of the dominant kernels from the committed
-    ncu --set full captures (profiles/<latest round>/traffic.json)."""
+    ncu --set full captures (profiles/<latest round>/traffic.json), only from
+    captures taken at the benched grid size n (a smaller grid's state fits the
+    126 MB L2 and would under-report DRAM traffic)."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")))
     if not files:
         return {}
     try:
-        return json.load(open(files[-1]))
+        tr = json.load(open(files[-1]))
     except (OSError, ValueError):
         return {}
+    return {k: v for k, v in tr.items() if isinstance(v, dict) and v.get("grid") == n}
 
 
 def cpu_reference_sample(cfg_name, n_sample, steps, threads):
@@ -292,7 +295,7 @@ def run_ours(args):
     stencil_bytes = 2.0 * 8 * (S + 1) * ncell_local * computed_slow * args.steps
     stencil_gbs = stencil_bytes / (slow_ms * 1e-3) / 1e9 if slow_ms > 0 else None
     pk = peaks()
-    tr = ncu_traffic()
+    tr = ncu_traffic(n)
 
     # ---------------- end-to-end through the host-buffer C-ABI ----------------
     e2e = None
@@ -400,6 +403,24 @@ def workload_text(args, cfg, n, n0l, H):
             f"Arrhenius), {method}, H={H:g}")
 
 
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1) outside a launcher: start N ranks
+    with torch.distributed.run on this node (one process per GPU) and return
+    their exit code.  Refuses loudly when fewer than N GPUs are visible."""
+    import torch
+    have = torch.cuda.device_count()
+    if args.impl != "reference" and have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) are visible")
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -417,6 +438,11 @@ def main():
     ap.add_argument("--slab-of", type=int, default=0,
                     help="N=1: run one rank's slab of an N-GPU decomposition (e.g. C5: 8)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but the launcher started {world} rank(s)")
     if args.impl == "reference":
         run_reference(args)
     else:
