@@ -68,6 +68,18 @@ typedef struct mr_ctx mr_ctx;
 
 /* ---------------- context / grid ---------------- */
 int mr_ctx_create(int device, mr_ctx** out);
+/* One process, several GPUs (the reference's single-threaded caller driving a
+ * multi-GPU run): a DOMAIN context owning one slab context per listed device
+ * (a device may repeat).  mr_grid_set on it (i0 = 0, n0_local = n0) splits
+ * axis 0 into equal slabs in device order; every setup call is applied to all
+ * slabs; upload/download scatter/gather the reference's species-major host
+ * layout; a step runs the stage plan on every device, each slab on its own
+ * stream, with the ghost planes copied peer-to-peer (cudaMemcpyPeerAsync over
+ * NVLink, ordered by events) and the IMEX dot products summed in slab order --
+ * bitwise the result of the same slabs as in-process virtual ranks.  Not
+ * available on a domain: mr_state_device_ptr, the device-pointer reductions,
+ * mr_mri_step_async, mr_comm_init.  mr_ctx_destroy frees the slabs. */
+int mr_ctx_create_multi(const int* devices, int n, mr_ctx** out);
 void mr_ctx_destroy(mr_ctx* ctx);
 const char* mr_last_error(const mr_ctx* ctx);
 int mr_version(void);

@@ -35,6 +35,17 @@ public:
     if (mr_ctx_create(device, &ctx_) != MR_OK || !ctx_)
       throw std::runtime_error("multirate::b200: no usable CUDA device (no CPU fallback)");
   }
+  // Several GPUs of this process (mr_ctx_create_multi): the grid is
+  // slab-decomposed along axis 0 over `devices` in order, the ghost planes
+  // travel peer-to-peer over NVLink, and every call below -- including
+  // mri_integrate -- drives all of them; the results are bitwise those of
+  // one GPU.
+  explicit Device(const std::vector<int>& devices)
+  {
+    if (devices.empty() ||
+        mr_ctx_create_multi(devices.data(), (int)devices.size(), &ctx_) != MR_OK || !ctx_)
+      throw std::runtime_error("multirate::b200: no usable CUDA devices (no CPU fallback)");
+  }
   ~Device() { mr_ctx_destroy(ctx_); }
   Device(const Device&) = delete;
   Device& operator=(const Device&) = delete;

@@ -77,6 +77,7 @@ def lib():
     vp = C.c_void_p
     sig = {
         "mr_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+        "mr_ctx_create_multi": (C.c_int, [_ip, C.c_int, C.POINTER(vp)]),
         "mr_ctx_destroy": (None, [vp]),
         "mr_last_error": (C.c_char_p, [vp]),
         "mr_version": (C.c_int, []),
@@ -234,14 +235,20 @@ def _bind_process_nccl():
 
 
 class Context:
-    """One device-resident MRI problem (one slab of the grid)."""
+    """One device-resident MRI problem (one slab of the grid) -- or, given a
+    list of devices, a multi-device domain (mr_ctx_create_multi): the grid is
+    split into slabs over the devices and every call drives all of them."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device=0):
         L = lib()
         h = C.c_void_p()
-        rc = L.mr_ctx_create(device, C.byref(h))
+        if isinstance(device, (list, tuple)):
+            devs = np.ascontiguousarray(device, dtype=np.int32)
+            rc = L.mr_ctx_create_multi(_p(devs, _ip), len(devs), C.byref(h))
+        else:
+            rc = L.mr_ctx_create(device, C.byref(h))
         if rc:
-            raise CudaError(f"mr_ctx_create failed (rc={rc}): no usable B200 / CUDA device")
+            raise CudaError(f"context creation failed (rc={rc}): no usable B200 / CUDA device")
         self.h = h
         self.L = L
         self.dof = 0

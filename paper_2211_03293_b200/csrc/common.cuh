@@ -87,7 +87,9 @@ struct ChemParams {
 };
 
 struct ChemCfg {
-  int NW, SPL;  // warps per cell group (slots), components per thread
+  int NW, SPL;  // warps per block (slots), components per thread
+  int cpt;      // cells per thread: 1 (kernels_chem.cuh, 32 cells per block) or
+                // 2 (kernels_chem2.cuh, 64 cells per block)
   bool subdiag;
   int nstage;  // inner table stages (non-subdiagonal tables: stage accumulators)
   int ndeg;
@@ -153,12 +155,11 @@ cudaError_t launch_fast_rhs(const ChainCfg& cfg, const double* y, double* out, s
                             int ncomp, const LinDev& lin, cudaStream_t st);
 
 int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int ndeg);
-int chem_chunking(int NW, int S, int R, size_t blob_bytes, int* rc, int* nchunk);
+int chem_chunking(const ChemCfg& cfg, int S, int R, size_t blob_bytes, int* rc, int* nchunk);
 cudaError_t launch_chem_chain(const ChemCfg& cfg, const ChainArgs& a, const ChemParams& P,
                               cudaStream_t st);
 cudaError_t launch_chem_rhs(const ChemCfg& cfg, const double* y, double* out, size_t ncell,
                             int ncomp, const ChemParams& P, cudaStream_t st);
-size_t chem_smem_bytes(const ChemCfg& cfg, int S, int R);
 
 cudaError_t launch_update(const double* y_in, double* y_out, int nref, const double* const* f,
                           const double* coef, size_t n, int mri_stage,

@@ -230,6 +230,16 @@ struct mr_ctx {
     const double* ycur = nullptr;
   } pending;
   cudaEvent_t ev_async_in = nullptr, ev_async_out = nullptr;
+  // multi-device domain (mr_ctx_create_multi): a domain context owns one slab
+  // context per device, slabs along axis 0 in device order.  A slab of a
+  // domain launches on its own stream and device; its neighbours' copies of
+  // its ghost planes and the slab-ordered dot products are ordered by events.
+  std::vector<mr_ctx*> slabs;
+  bool in_domain = false;
+  cudaEvent_t ev_send = nullptr;  // this slab's ghost planes are packed
+  cudaEvent_t ev_recv = nullptr;  // this slab has copied its neighbours' planes
+  cudaEvent_t ev_dot = nullptr;   // this slab's dot-product partial is final
+  bool recv_recorded = false;
 };
 
 namespace {
@@ -238,6 +248,15 @@ int set_err(mr_ctx* c, int code, const std::string& msg)
 {
   if (c) c->err = msg;
   return code;
+}
+
+// stream / device of slab c inside a step whose shared stream is st: the slabs
+// of a multi-device domain each run on their own stream and device, the
+// in-process virtual ranks of one device share the first slab's stream
+inline cudaStream_t sst(const mr_ctx* c, cudaStream_t st) { return c->in_domain ? c->stream : st; }
+inline void sdev(const mr_ctx* c)
+{
+  if (c->in_domain) cudaSetDevice(c->device);
 }
 
 #define MR_CUDA_TRY(ctx, call)                                                            \
@@ -567,13 +586,21 @@ int nccl_halo_exchange(mr_ctx* c, cudaStream_t st)
 int exchange_halos(mr_ctx** cs, int n, const double* const* ycur, const double** lo,
                    const double** hi, cudaStream_t st)
 {
+  const bool dom = cs[0]->in_domain && n > 1;
   for (int r = 0; r < n; ++r) {
     mr_ctx* c = cs[r];
+    sdev(c);
     int rc = ensure_halo(c);
     if (rc) return rc;
+    if (dom && cs[(r + n - 1) % n]->recv_recorded) {
+      // the neighbours' copies of this slab's previous planes are done
+      MR_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, cs[(r + n - 1) % n]->ev_recv, 0));
+      MR_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, cs[(r + 1) % n]->ev_recv, 0));
+    }
     MR_CUDA_TRY(c, launch_halo_pack(ycur[r], c->send_lo, c->send_hi, c->ncomp, c->n0l, c->plane,
-                                    c->M, st));
+                                    c->M, sst(c, st)));
     c->launches++;
+    if (dom) MR_CUDA_TRY(c, cudaEventRecord(c->ev_send, c->stream));
   }
   if (n == 1 && !cs[0]->comm) {  // periodic single slab: own planes wrap around
     lo[0] = cs[0]->send_hi;
@@ -588,9 +615,13 @@ int exchange_halos(mr_ctx** cs, int n, const double* const* ycur, const double**
     hi[0] = c->recv_hi;
     return MR_OK;
   }
-  // in-process virtual ranks on one device: device-to-device copies
+  // several slabs in one process: each slab copies its neighbours' packed
+  // planes -- peer-to-peer over NVLink between the GPUs of a multi-device
+  // domain (after the neighbours' pack events), device-to-device on the one
+  // shared stream of in-process virtual ranks
   for (int r = 0; r < n; ++r) {
     mr_ctx* c = cs[r];
+    sdev(c);
     if (!c->recv_lo) {
       MR_CUDA_TRY(c, cudaMalloc(&c->recv_lo, c->halo_elems * sizeof(double)));
       MR_CUDA_TRY(c, cudaMalloc(&c->recv_hi, c->halo_elems * sizeof(double)));
@@ -600,10 +631,20 @@ int exchange_halos(mr_ctx** cs, int n, const double* const* ycur, const double**
     mr_ctx* c = cs[r];
     mr_ctx* L = cs[(r - 1 + n) % n];
     mr_ctx* Rr = cs[(r + 1) % n];
-    MR_CUDA_TRY(c, cudaMemcpyAsync(c->recv_lo, L->send_hi, c->halo_elems * sizeof(double),
-                                   cudaMemcpyDeviceToDevice, st));
-    MR_CUDA_TRY(c, cudaMemcpyAsync(c->recv_hi, Rr->send_lo, c->halo_elems * sizeof(double),
-                                   cudaMemcpyDeviceToDevice, st));
+    sdev(c);
+    const cudaStream_t s2 = sst(c, st);
+    const size_t bytes = c->halo_elems * sizeof(double);
+    if (dom) {
+      MR_CUDA_TRY(c, cudaStreamWaitEvent(s2, L->ev_send, 0));
+      MR_CUDA_TRY(c, cudaStreamWaitEvent(s2, Rr->ev_send, 0));
+      MR_CUDA_TRY(c, cudaMemcpyPeerAsync(c->recv_lo, c->device, L->send_hi, L->device, bytes, s2));
+      MR_CUDA_TRY(c, cudaMemcpyPeerAsync(c->recv_hi, c->device, Rr->send_lo, Rr->device, bytes, s2));
+      MR_CUDA_TRY(c, cudaEventRecord(c->ev_recv, s2));
+      c->recv_recorded = true;
+    } else {
+      MR_CUDA_TRY(c, cudaMemcpyAsync(c->recv_lo, L->send_hi, bytes, cudaMemcpyDeviceToDevice, s2));
+      MR_CUDA_TRY(c, cudaMemcpyAsync(c->recv_hi, Rr->send_lo, bytes, cudaMemcpyDeviceToDevice, s2));
+    }
     lo[r] = c->recv_lo;
     hi[r] = c->recv_hi;
   }
@@ -658,7 +699,9 @@ int eval_slow(mr_ctx** cs, int n, const double* const* ycur, double* const* outs
 {
   if (cs[0]->slow_kind == SK_LINEAR) {
     for (int r = 0; r < n; ++r) {
-      MR_CUDA_TRY(cs[r], launch_slow_linear(ycur[r], outs[r], cs[r]->ncell, cs[r]->slowA, st));
+      sdev(cs[r]);
+      MR_CUDA_TRY(cs[r], launch_slow_linear(ycur[r], outs[r], cs[r]->ncell, cs[r]->slowA,
+                                            sst(cs[r], st)));
       cs[r]->launches++;
     }
     return MR_OK;
@@ -705,7 +748,9 @@ int eval_slow(mr_ctx** cs, int n, const double* const* ycur, double* const* outs
   int rc = exchange_halos(cs, n, ycur, lo.data(), hi.data(), st);
   if (rc) return rc;
   for (int r = 0; r < n; ++r) {
-    MR_CUDA_TRY(cs[r], launch_stencil(stencil_args(cs[r], ycur[r], outs[r], lo[r], hi[r]), st));
+    sdev(cs[r]);
+    MR_CUDA_TRY(cs[r], launch_stencil(stencil_args(cs[r], ycur[r], outs[r], lo[r], hi[r]),
+                                      sst(cs[r], st)));
     cs[r]->launches++;
   }
   return MR_OK;
@@ -796,8 +841,10 @@ int eval_implicit(mr_ctx** cs, int n, const double* const* ycur, double* const* 
   int rc = exchange_halos(cs, n, ycur, lo.data(), hi.data(), st);
   if (rc) return rc;
   for (int r = 0; r < n; ++r) {
+    sdev(cs[r]);
     MR_CUDA_TRY(cs[r], launch_lap7(0, lap_args(cs[r], 0.0), ycur[r], lo[r], hi[r], nullptr,
-                                   nullptr, outs[r], nullptr, nullptr, nullptr, nullptr, st));
+                                   nullptr, outs[r], nullptr, nullptr, nullptr, nullptr,
+                                   sst(cs[r], st)));
     cs[r]->launches++;
   }
   return MR_OK;
@@ -808,9 +855,36 @@ int eval_implicit(mr_ctx** cs, int n, const double* const* ycur, double* const* 
 int dot_finalize(mr_ctx** cs, int n, int slot, cudaStream_t st, bool second = false)
 {
   for (int r = 0; r < n; ++r) {
+    sdev(cs[r]);
     MR_CUDA_TRY(cs[r], launch_part_sum(second ? cs[r]->cg_part2 : cs[r]->cg_part, cs[r]->cg_sc,
-                                       slot, st));
+                                       slot, sst(cs[r], st)));
     cs[r]->launches++;
+  }
+  if (n > 1 && cs[0]->in_domain) {
+    // multi-device: gather the slab values on the first slab's device, sum
+    // them in slab order there (the order of scalar_combine_kernel, so the
+    // result is bitwise that of the virtual ranks) and copy the sum back
+    mr_ctx* c0 = cs[0];
+    for (int r = 0; r < n; ++r) {
+      sdev(cs[r]);
+      MR_CUDA_TRY(cs[r], cudaEventRecord(cs[r]->ev_dot, cs[r]->stream));
+    }
+    sdev(c0);
+    for (int r = 0; r < n; ++r) {
+      MR_CUDA_TRY(c0, cudaStreamWaitEvent(c0->stream, cs[r]->ev_dot, 0));
+      MR_CUDA_TRY(c0, cudaMemcpyPeerAsync(c0->cg_gather + r, c0->device, cs[r]->cg_sc + slot,
+                                          cs[r]->device, sizeof(double), c0->stream));
+    }
+    MR_CUDA_TRY(c0, launch_gathered_sum(c0->cg_gather, n, c0->cg_sc, slot, c0->stream));
+    c0->launches++;
+    MR_CUDA_TRY(c0, cudaEventRecord(c0->ev_dot, c0->stream));
+    for (int r = 1; r < n; ++r) {
+      sdev(cs[r]);
+      MR_CUDA_TRY(cs[r], cudaStreamWaitEvent(cs[r]->stream, c0->ev_dot, 0));
+      MR_CUDA_TRY(cs[r], cudaMemcpyPeerAsync(cs[r]->cg_sc + slot, cs[r]->device, c0->cg_sc + slot,
+                                             c0->device, sizeof(double), cs[r]->stream));
+    }
+    return MR_OK;
   }
   if (n > 1) {
     std::vector<double*> scs(n);
@@ -853,17 +927,19 @@ int newton_pcg(mr_ctx** cs, int n, int i, double gamma, double* const* fI_out,
     if (rc) return rc;
     for (int r = 0; r < n; ++r) {
       mr_ctx* c = cs[r];
+      sdev(c);
       MR_CUDA_TRY(c, launch_lap7(1, lap_args(c, gamma), c->y_work, lo[r], hi[r], c->cg_known,
                                  c->newton_w, c->cg_r, c->cg_z, c->cg_p, c->cg_part, c->cg_part2,
-                                 st));
+                                 sst(c, st)));
       c->launches++;
       c->solve_evals[i]++;
     }
     rc = dot_finalize(cs, n, 3, st);
     if (rc) return rc;
+    sdev(c0);
     MR_CUDA_TRY(c0, cudaMemcpyAsync(c0->h_red, c0->cg_sc + 3, sizeof(double),
-                                    cudaMemcpyDeviceToHost, st));
-    MR_CUDA_TRY(c0, cudaStreamSynchronize(st));
+                                    cudaMemcpyDeviceToHost, sst(c0, st)));
+    MR_CUDA_TRY(c0, cudaStreamSynchronize(sst(c0, st)));
     const double wrms = std::sqrt(c0->h_red[0] / nglob);
     if (!std::isfinite(wrms)) break;
     if (wrms <= target) {
@@ -879,24 +955,27 @@ int newton_pcg(mr_ctx** cs, int n, int i, double gamma, double* const* fI_out,
       if (rc) return rc;
       for (int r = 0; r < n; ++r) {
         mr_ctx* c = cs[r];
+        sdev(c);
         MR_CUDA_TRY(c, launch_lap7(2, lap_args(c, gamma), c->cg_p, lo[r], hi[r], nullptr, nullptr,
-                                   c->cg_q, nullptr, nullptr, c->cg_part, nullptr, st));
+                                   c->cg_q, nullptr, nullptr, c->cg_part, nullptr, sst(c, st)));
         c->launches++;
       }
       rc = dot_finalize(cs, n, 1, st);  // pAp
       if (rc) return rc;
       for (int r = 0; r < n; ++r) {
         mr_ctx* c = cs[r];
+        sdev(c);
         MR_CUDA_TRY(c, launch_cg_update(c->dof, lap_args(c, gamma).dg, c->cg_sc, c->y_work,
-                                        c->cg_r, c->cg_z, c->cg_p, c->cg_q, c->cg_part, st));
+                                        c->cg_r, c->cg_z, c->cg_p, c->cg_q, c->cg_part, sst(c, st)));
         c->launches++;
       }
       rc = dot_finalize(cs, n, 2, st);  // rz_new
       if (rc) return rc;
       for (int r = 0; r < n; ++r) {
         mr_ctx* c = cs[r];
-        MR_CUDA_TRY(c, launch_cg_p(c->dof, c->cg_sc, c->cg_p, c->cg_z, st));
-        MR_CUDA_TRY(c, launch_scalar_copy(c->cg_sc, 0, 2, st));
+        sdev(c);
+        MR_CUDA_TRY(c, launch_cg_p(c->dof, c->cg_sc, c->cg_p, c->cg_z, sst(c, st)));
+        MR_CUDA_TRY(c, launch_scalar_copy(c->cg_sc, 0, 2, sst(c, st)));
         c->launches += 2;
       }
     }
@@ -908,8 +987,9 @@ int newton_pcg(mr_ctx** cs, int n, int i, double gamma, double* const* fI_out,
   }
   for (int r = 0; r < n; ++r) {
     mr_ctx* c = cs[r];
+    sdev(c);
     MR_CUDA_TRY(c, launch_recover_fi(c->dof, gamma, c->y_work, c->cg_known, fI_out[r], i, c->d_fail,
-                                     st));
+                                     sst(c, st)));
     c->launches++;
   }
   return MR_OK;
@@ -923,6 +1003,7 @@ int solve_stage(mr_ctx** cs, int n, int i, double t, double H, const Plan& plan,
   const double gamma = H * cs[0]->cp.gbar[i][i];
   for (int r = 0; r < n; ++r) {
     mr_ctx* c = cs[r];
+    sdev(c);
     int rc = ensure_cg(c);
     if (rc) return rc;
     ChainStageDev sd;
@@ -930,9 +1011,9 @@ int solve_stage(mr_ctx** cs, int n, int i, double t, double H, const Plan& plan,
     const double* f[MR_MAXREF];
     for (int q = 0; q < sd.nref; ++q) f[q] = c->slots[sd.ref_slot[q]];
     MR_CUDA_TRY(c, launch_update(ycur[r], c->cg_known, sd.nref, f, sd.coef[0], c->dof, i,
-                                 c->d_fail, st));
+                                 c->d_fail, sst(c, st)));
     MR_CUDA_TRY(c, cudaMemcpyAsync(c->y_work, c->cg_known, c->dof * sizeof(double),
-                                   cudaMemcpyDeviceToDevice, st));
+                                   cudaMemcpyDeviceToDevice, sst(c, st)));
     c->launches++;
     ycur[r] = c->y_work;
   }
@@ -957,6 +1038,7 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
   if (fail_stage) *fail_stage = -1;
   if (!(H > 0.0)) return set_err(c0, MR_CONTRACT, "mri_step: H must be positive");
   for (int r = 0; r < n; ++r) {
+    sdev(cs[r]);
     int rc = check_ready(cs[r]);
     if (rc) return rc;
     rc = ensure_state(cs[r]);
@@ -982,6 +1064,7 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
       return set_err(c0, MR_CONTRACT, "coupling stage references more slow values than the device plan holds");
   }
   for (int r = 0; r < n; ++r) {
+    sdev(cs[r]);
     int rc = ensure_slots(cs[r], plan.nslots);
     if (rc) return rc;
   }
@@ -994,8 +1077,11 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
   } else if (chain_pick(&cfg, c0->fast_kind, c0->ncomp, c0->tab.s, ndeg_of(c0))) {
     return set_err(c0, MR_CONTRACT, "unsupported component count / table for the fused IVP kernel");
   }
-  for (int r = 0; r < n; ++r)
-    MR_CUDA_TRY(cs[r], cudaMemsetAsync(cs[r]->d_fail, 0xFF, sizeof(unsigned long long), st));
+  for (int r = 0; r < n; ++r) {
+    sdev(cs[r]);
+    MR_CUDA_TRY(cs[r], cudaMemsetAsync(cs[r]->d_fail, 0xFF, sizeof(unsigned long long),
+                                       sst(cs[r], st)));
+  }
 
   std::vector<const double*> ycur(n);
   std::vector<double*> outs(n);
@@ -1037,12 +1123,13 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
     } else if (o.type == Op::UPDATE) {
       for (int r = 0; r < n; ++r) {
         mr_ctx* c = cs[r];
+        sdev(c);
         ChainStageDev sd;
         fill_chain_stage(c, o.stage, t, H, plan, sd);
         const double* f[MR_MAXREF];
         for (int q = 0; q < sd.nref; ++q) f[q] = c->slots[sd.ref_slot[q]];
         MR_CUDA_TRY(c, launch_update(ycur[r], c->y_work, sd.nref, f, sd.coef[0], c->dof, o.stage,
-                                     c->d_fail, st));
+                                     c->d_fail, sst(c, st)));
         c->launches++;
         ycur[r] = c->y_work;
       }
@@ -1061,10 +1148,11 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
         a.ncell = c->ncell;
         a.ncomp = c->ncomp;
         a.fail = c->d_fail;
+        sdev(c);
         if (c->fast_kind == FK_CHEM)
-          MR_CUDA_TRY(c, launch_chem_chain(ccfg, a, *c->chemP, st));
+          MR_CUDA_TRY(c, launch_chem_chain(ccfg, a, *c->chemP, sst(c, st)));
         else
-          MR_CUDA_TRY(c, launch_chain(cfg, a, c->fastA, st));
+          MR_CUDA_TRY(c, launch_chain(cfg, a, c->fastA, sst(c, st)));
         c->launches++;
         ycur[r] = c->y_work;
       }
@@ -1077,8 +1165,9 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
     MR_NCCL_TRY(c0, AllReduce(c0->d_fail, c0->d_fail, 1, ncclUint64, ncclMin, c0->comm, st));
   }
   for (int r = 0; r < n; ++r) {
+    sdev(cs[r]);
     MR_CUDA_TRY(cs[r], cudaMemcpyAsync(cs[r]->h_fail, cs[r]->d_fail, sizeof(unsigned long long),
-                                       cudaMemcpyDeviceToHost, st));
+                                       cudaMemcpyDeviceToHost, sst(cs[r], st)));
   }
   if (async) {
     mr_ctx::Pending& pd = c0->pending;
@@ -1104,7 +1193,11 @@ int domain_finish(mr_ctx** cs, int n, const Plan& plan, double t, double H, int 
 {
   mr_ctx* c0 = cs[0];
   if (fail_stage) *fail_stage = -1;
-  MR_CUDA_TRY(c0, cudaStreamSynchronize(c0->stream));
+  for (int r = 0; r < n; ++r) {
+    if (!cs[r]->in_domain && r > 0) break;  // virtual ranks share the first slab's stream
+    sdev(cs[r]);
+    MR_CUDA_TRY(c0, cudaStreamSynchronize(cs[r]->stream));
+  }
   unsigned long long key = MR_NO_FAIL;
   for (int r = 0; r < n; ++r) key = std::min(key, *cs[r]->h_fail);
   key = std::min(key, host_key);
@@ -1227,6 +1320,135 @@ static int pending_guard(mr_ctx* c)
   return MR_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// multi-device domain helpers (mr_ctx_create_multi)
+// ---------------------------------------------------------------------------
+// f applied to every slab of a domain; the first failure's message becomes the
+// domain's
+template <class F>
+static int for_slabs(mr_ctx* d, F&& f)
+{
+  for (mr_ctx* sl : d->slabs) {
+    const int rc = f(sl);
+    if (rc) return set_err(d, rc, sl->err);
+  }
+  return MR_OK;
+}
+
+// after a multi-slab call: the first slab carries the step's error message
+static int domain_rc(mr_ctx* d, int rc)
+{
+  if (rc) d->err = d->slabs[0]->err;
+  return rc;
+}
+
+// host <-> slab copies of a domain-wide species-major buffer
+// Y[comp][global cell]: slab r's component k is one contiguous chunk at
+// comp * ncell_global + i0 * plane, so each slab is one 2D copy (ncomp rows)
+static int domain_copy(mr_ctx* d, const double* host_in, double* host_out, double* const* dev_bufs,
+                bool to_dev)
+{
+  const size_t gpitch = d->ncell * sizeof(double);
+  for (size_t r = 0; r < d->slabs.size(); ++r) {
+    mr_ctx* sl = d->slabs[r];
+    cudaSetDevice(sl->device);
+    const size_t lpitch = sl->ncell * sizeof(double);
+    const size_t off = (size_t)sl->i0 * sl->plane;
+    if (to_dev)
+      MR_CUDA_TRY(d, cudaMemcpy2DAsync(dev_bufs[r], lpitch, host_in + off, gpitch, lpitch,
+                                       (size_t)sl->ncomp, cudaMemcpyHostToDevice, sl->stream));
+    else
+      MR_CUDA_TRY(d, cudaMemcpy2DAsync(host_out + off, gpitch, dev_bufs[r], lpitch, lpitch,
+                                       (size_t)sl->ncomp, cudaMemcpyDeviceToHost, sl->stream));
+  }
+  for (mr_ctx* sl : d->slabs) {
+    cudaSetDevice(sl->device);
+    MR_CUDA_TRY(d, cudaStreamSynchronize(sl->stream));
+  }
+  return MR_OK;
+}
+
+// a slab's share of a domain-wide host array (species-major), as a vector
+static std::vector<double> domain_slice(const mr_ctx* d, const mr_ctx* sl, const double* host)
+{
+  std::vector<double> v(sl->dof);
+  const size_t off = (size_t)sl->i0 * sl->plane;
+  for (int k = 0; k < sl->ncomp; ++k)
+    std::memcpy(v.data() + (size_t)k * sl->ncell, host + (size_t)k * d->ncell + off,
+                sl->ncell * sizeof(double));
+  return v;
+}
+
+// the contexts a step runs over: the slabs of a domain, or the context itself
+static std::vector<mr_ctx*> members(mr_ctx* c)
+{
+  return c->slabs.empty() ? std::vector<mr_ctx*>{c} : c->slabs;
+}
+
+// one RHS of a domain-wide host vector: scatter into each slab's scratch,
+// evaluate (kind 0 fast, 1 slow, 2 implicit), gather (Mode A, multi-GPU)
+// one fast-partition RHS evaluation between device buffers
+static int eval_fast_dev(mr_ctx* c, const double* in, double* out, cudaStream_t st)
+{
+  if (c->fast_kind == FK_CHEM) {
+    ChemCfg ccfg;
+    TableDev t4{};
+    t4.s = 4;
+    if (chem_pick(&ccfg, c->ncomp, c->S, c->R, t4, 1))
+      return set_err(c, MR_CONTRACT, "unsupported mechanism size");
+    MR_CUDA_TRY(c, launch_chem_rhs(ccfg, in, out, c->ncell, c->ncomp, *c->chemP, st));
+  } else {
+    ChainCfg cfg;
+    if (chain_pick(&cfg, c->fast_kind, c->ncomp, 4, 1))
+      return set_err(c, MR_CONTRACT, "unsupported component count");
+    MR_CUDA_TRY(c, launch_fast_rhs(cfg, in, out, c->ncell, c->ncomp, c->fastA, st));
+  }
+  c->launches++;
+  return MR_OK;
+}
+static int domain_rhs(mr_ctx* d, int kind, const double* y, double* out)
+{
+  const int n = (int)d->slabs.size();
+  std::vector<double*> in(n), o(n);
+  std::vector<const double*> ci(n);
+  for (int r = 0; r < n; ++r) {
+    mr_ctx* sl = d->slabs[r];
+    cudaSetDevice(sl->device);
+    if (!sl->scr_in) MR_CUDA_TRY(d, cudaMalloc(&sl->scr_in, sl->dof * sizeof(double)));
+    if (!sl->scr_out) MR_CUDA_TRY(d, cudaMalloc(&sl->scr_out, sl->dof * sizeof(double)));
+    in[r] = sl->scr_in;
+    ci[r] = sl->scr_in;
+    o[r] = sl->scr_out;
+  }
+  int rc = domain_copy(d, y, nullptr, in.data(), true);
+  if (rc) return rc;
+  if (kind == 0) {
+    for (int r = 0; r < n; ++r) {
+      cudaSetDevice(d->slabs[r]->device);
+      rc = eval_fast_dev(d->slabs[r], in[r], o[r], d->slabs[r]->stream);
+      if (rc) return domain_rc(d, rc);
+    }
+  } else if (kind == 1) {
+    rc = eval_slow(d->slabs.data(), n, ci.data(), o.data(), d->slabs[0]->stream);
+    if (rc) return domain_rc(d, rc);
+  } else {
+    rc = eval_implicit(d->slabs.data(), n, ci.data(), o.data(), d->slabs[0]->stream);
+    if (rc) return domain_rc(d, rc);
+  }
+  return domain_copy(d, nullptr, out, o.data(), false);
+}
+
+#define MR_FORWARD(c, expr)                                            \
+  do {                                                                 \
+    if (!(c)->slabs.empty()) return for_slabs((c), [&](mr_ctx* sl_) { return (expr); }); \
+  } while (0)
+#define MR_NOT_ON_DOMAIN(c, what)                                                          \
+  do {                                                                                     \
+    if (!(c)->slabs.empty())                                                               \
+      return set_err((c), MR_CONTRACT, std::string(what) + ": not available on a multi-device domain"); \
+  } while (0)
+
 // ===========================================================================
 // C-ABI
 // ===========================================================================
@@ -1256,9 +1478,59 @@ int mr_ctx_create(int device, mr_ctx** out)
   return MR_OK;
 }
 
+// one process, several GPUs (SURVEY.md 8(b) mr_ctx_create(devices, n)): a
+// domain context owning one slab context per listed device
+int mr_ctx_create_multi(const int* devices, int n, mr_ctx** out)
+{
+  if (!out || !devices || n < 1) return MR_CONTRACT;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return MR_CUDA;
+  for (int i = 0; i < n; ++i)
+    if (devices[i] < 0 || devices[i] >= ndev) return MR_CONTRACT;
+  mr_ctx* d = new mr_ctx();
+  d->device = devices[0];
+  for (int i = 0; i < n; ++i) {
+    mr_ctx* sl = nullptr;
+    const int rc = mr_ctx_create(devices[i], &sl);
+    if (rc) {
+      mr_ctx_destroy(d);
+      return rc;
+    }
+    d->slabs.push_back(sl);
+    sl->in_domain = true;
+    cudaSetDevice(sl->device);
+    if (cudaEventCreateWithFlags(&sl->ev_send, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&sl->ev_recv, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&sl->ev_dot, cudaEventDisableTiming) != cudaSuccess) {
+      mr_ctx_destroy(d);
+      return MR_CUDA;
+    }
+  }
+  d->stream = d->slabs[0]->stream;  // mr_stream(): the first slab's stream
+  // direct NVLink copies between the GPUs that exchange ghost planes (ring
+  // neighbours) and dot-product scalars (with the first slab's GPU)
+  for (int i = 0; i < n; ++i)
+    for (int j : {(i + 1) % n, (i + n - 1) % n, 0}) {
+      const int a = devices[i], b = devices[j];
+      int ok = 0;
+      if (a == b || cudaDeviceCanAccessPeer(&ok, a, b) != cudaSuccess || !ok) continue;
+      cudaSetDevice(a);
+      if (cudaDeviceEnablePeerAccess(b, 0) != cudaSuccess) cudaGetLastError();  // already enabled
+    }
+  cudaSetDevice(devices[0]);
+  *out = d;
+  return MR_OK;
+}
+
 void mr_ctx_destroy(mr_ctx* c)
 {
   if (!c) return;
+  if (!c->slabs.empty() || (!c->stream && !c->in_domain)) {  // a domain: its slabs own everything
+    for (mr_ctx* sl : c->slabs) mr_ctx_destroy(sl);
+    delete c;
+    return;
+  }
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   free_state(c);
@@ -1281,6 +1553,9 @@ void mr_ctx_destroy(mr_ctx* c)
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->ev_pack) cudaEventDestroy(c->ev_pack);
   if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  if (c->ev_send) cudaEventDestroy(c->ev_send);
+  if (c->ev_recv) cudaEventDestroy(c->ev_recv);
+  if (c->ev_dot) cudaEventDestroy(c->ev_dot);
   delete c;
 }
 
@@ -1293,6 +1568,18 @@ int mr_grid_set(mr_ctx* c, int n0, int n1, int n2, int n_comp, double length, in
   if (n0 < 1 || n1 < 1 || n2 < 1 || n_comp < 1 || !(length > 0.0) || i0 < 0 || n0_local < 1 ||
       i0 + n0_local > n0)
     return set_err(c, MR_CONTRACT, "mr_grid_set: bad grid");
+  if (!c->slabs.empty()) {  // a domain owns the whole grid; equal slabs in device order
+    const int P = (int)c->slabs.size();
+    if (i0 != 0 || n0_local != n0 || n0 < P)
+      return set_err(c, MR_CONTRACT,
+                     "mr_grid_set: a multi-device domain owns the whole grid (i0 = 0, n0_local = n0 >= devices)");
+    const int base = n0 / P, rem = n0 % P;
+    for (int r = 0; r < P; ++r) {
+      const int rc = mr_grid_set(c->slabs[r], n0, n1, n2, n_comp, length, r * base + std::min(r, rem),
+                                 base + (r < rem ? 1 : 0));
+      if (rc) return set_err(c, rc, c->slabs[r]->err);
+    }
+  }
   cudaSetDevice(c->device);
   free_state(c);
   c->n0 = n0; c->n1 = n1; c->n2 = n2; c->ncomp = n_comp; c->length = length;
@@ -1308,6 +1595,7 @@ int mr_coupling_load(mr_ctx* c, int s, int n_deg, const double* cc, const int* k
                      const double* gamma, const double* omega)
 {
   if (int g = pending_guard(c)) return g;
+  MR_FORWARD(c, mr_coupling_load(sl_, s, n_deg, cc, kind, gamma, omega));
   if (!c || !cc || !kind || s < 2 || s > kMaxStages || n_deg < 1 || n_deg > 8)
     return set_err(c, MR_CONTRACT, "mr_coupling_load: bad arguments");
   Coupling cp;
@@ -1334,6 +1622,7 @@ int mr_coupling_load_text(mr_ctx* c, const char* text)
 {
   if (!c || !text) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  MR_FORWARD(c, mr_coupling_load_text(sl_, text));
   Coupling cp;
   std::string err;
   int rc = read_coupling_text(text, cp, err);
@@ -1348,6 +1637,7 @@ int mr_coupling_load_text(mr_ctx* c, const char* text)
 int mr_table_load(mr_ctx* c, int s, const double* A, const double* b, const double* cc)
 {
   if (int g = pending_guard(c)) return g;
+  MR_FORWARD(c, mr_table_load(sl_, s, A, b, cc));
   if (!c || !A || !b || !cc || s < 1 || s > MR_MAXS)
     return set_err(c, MR_CONTRACT, "mr_table_load: bad arguments");
   TableDev t{};
@@ -1369,6 +1659,7 @@ int mr_table_load(mr_ctx* c, int s, const double* A, const double* b, const doub
 int mr_set_substeps(mr_ctx* c, int m)
 {
   if (int g = pending_guard(c)) return g;
+  MR_FORWARD(c, mr_set_substeps(sl_, m));
   if (!c || m < 1) return set_err(c, MR_CONTRACT, "m must be >= 1");
   c->m = m;
   return MR_OK;
@@ -1378,6 +1669,7 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
                       const double* reactions, const int* rspecies)
 {
   if (int g = pending_guard(c)) return g;
+  MR_FORWARD(c, mr_fast_chemistry(sl_, S, R, rho, species, reactions, rspecies));
   if (!c || S < 1 || R < 1 || !(rho > 0.0) || !species || !reactions || !rspecies)
     return set_err(c, MR_CONTRACT, "mr_fast_chemistry: bad arguments");
   cudaSetDevice(c->device);
@@ -1465,7 +1757,7 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
                               4 * ((size_t)nnz + 2 * 3 * (size_t)S * MR_CHEM_MAXCHUNK) + 16;
     int rcz = 0, nch = 0;
     if (chem_pick(&lay, S + 1, S, R, t4, 1) ||
-        chem_chunking(lay.NW, S, R, blob_bound, &rcz, &nch))
+        chem_chunking(lay, S, R, blob_bound, &rcz, &nch))
       return set_err(c, MR_CONTRACT, "mechanism too large for the chemistry kernel's shared memory");
     P.rc = rcz;
     P.nchunk = nch;
@@ -1488,15 +1780,20 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
         load[best] += cost[k];
       }
     }
+    // shared-memory row sizes of the layout: one cell per thread (32-cell
+    // rows: (C, E') double2 rows of 512 B, D' and q rows of 256 B) or two
+    // cells per thread (64-cell rows of 512 B; C, E', D' separate tables at
+    // fixed distances, so every species offset is k * 512)
+    const unsigned prow = lay.cpt == 2 ? 512u : 256u, qrow = prow;
     std::vector<ChemRec> recs(R);
     for (int j = 0; j < R; ++j) {
       ChemRec& r = recs[j];
       std::memset(&r, 0, sizeof(r));
       r.lnA = rx[j].x; r.beta = rx[j].y; r.EaR = rx[j].z;
       r.r1o = (unsigned)rs[j].x * 512u; r.r2o = (unsigned)rs[j].y * 512u;
-      r.p1o = (unsigned)rs[j].z * 256u; r.p2o = (unsigned)rs[j].w * 256u;
+      r.p1o = (unsigned)rs[j].z * prow; r.p2o = (unsigned)rs[j].w * prow;
     }
-    const unsigned zero_off = (unsigned)rcz * 256u;  // all-zero row right after q
+    const unsigned zero_off = (unsigned)rcz * qrow;  // all-zero row right after q
     std::vector<unsigned> ents;
     for (int k = 0; k < S; ++k)
       for (int ch2 = 0; ch2 < nch; ++ch2) {
@@ -1509,7 +1806,7 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
             const int j = ent[q2] >> 1, prod = ent[q2] & 1;
             if ((prod == 1) != (sign == 0)) continue;
             if (j < ch2 * rcz || j >= (ch2 + 1) * rcz) continue;
-            ents.push_back((unsigned)(j - ch2 * rcz) * 256u);
+            ents.push_back((unsigned)(j - ch2 * rcz) * qrow);
           }
           while ((ents.size() - n0) % 4) ents.push_back(zero_off);
           n4[sign] = (unsigned short)((ents.size() - n0) / 4);
@@ -1553,6 +1850,7 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
 int mr_fast_linear(mr_ctx* c, const double* A)
 {
   if (int g = pending_guard(c)) return g;
+  MR_FORWARD(c, mr_fast_linear(sl_, A));
   if (!c || !A || !c->has_grid || c->ncomp > MR_MAXLIN)
     return set_err(c, MR_CONTRACT, "mr_fast_linear: needs grid with n_comp <= 8");
   c->fastA.n = c->ncomp;
@@ -1565,6 +1863,7 @@ int mr_fast_none(mr_ctx* c)
 {
   if (!c) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  MR_FORWARD(c, mr_fast_none(sl_));
   c->fast_kind = FK_NONE;
   return MR_OK;
 }
@@ -1573,6 +1872,7 @@ int mr_slow_stencil(mr_ctx* c, int order, double diffusion, const double* u, con
                     int nmax)
 {
   if (int g = pending_guard(c)) return g;
+  MR_FORWARD(c, mr_slow_stencil(sl_, order, diffusion, u, prof, nmax));
   if (!c || !c->has_grid || (order != 2 && order != 4 && order != 8) || diffusion < 0.0)
     return set_err(c, MR_CONTRACT, "mr_slow_stencil: bad arguments (order 2/4/8, grid first)");
   cudaSetDevice(c->device);
@@ -1607,6 +1907,7 @@ static int ensure_scratch(mr_ctx* c);
 int mr_slow_implicit_diffusion(mr_ctx* c, double d_impl, int cg_iters)
 {
   if (int g = pending_guard(c)) return g;
+  MR_FORWARD(c, mr_slow_implicit_diffusion(sl_, d_impl, cg_iters));
   if (!c || c->slow_kind != SK_STENCIL || !(d_impl >= 0.0) || cg_iters < 0)
     return set_err(c, MR_CONTRACT,
                    "mr_slow_implicit_diffusion: needs the stencil plugin, d_impl >= 0, cg_iters >= 0");
@@ -1620,6 +1921,14 @@ int mr_newton_config(mr_ctx* c, double tolerance, double safety, int max_iters,
                      const double* weights)
 {
   if (int g = pending_guard(c)) return g;
+  if (!c->slabs.empty()) {
+    if (weights && !c->has_grid) return set_err(c, MR_CONTRACT, "grid not set (mr_grid_set)");
+    return for_slabs(c, [&](mr_ctx* sl_) {
+      if (!weights) return mr_newton_config(sl_, tolerance, safety, max_iters, nullptr);
+      const std::vector<double> w = domain_slice(c, sl_, weights);
+      return mr_newton_config(sl_, tolerance, safety, max_iters, w.data());
+    });
+  }
   if (!c || !(tolerance > 0.0) || !(safety > 0.0) || safety > 1.0 || max_iters < 0)
     return set_err(c, MR_CONTRACT, "newton_solve: bad NewtonConfig");
   if (weights && !c->has_grid) return set_err(c, MR_CONTRACT, "grid not set (mr_grid_set)");
@@ -1640,6 +1949,11 @@ int mr_implicit_rhs(mr_ctx* c, double t, const double* y, double* out)
   (void)t;
   if (!c || !y || !out) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  if (!c->slabs.empty()) {
+    if (!c->slabs[0]->imex)
+      return set_err(c, MR_CONTRACT, "mr_implicit_rhs: no implicit partition configured");
+    return domain_rhs(c, 2, y, out);
+  }
   if (!c->imex) return set_err(c, MR_CONTRACT, "mr_implicit_rhs: no implicit partition configured");
   cudaSetDevice(c->device);
   int rc = ensure_scratch(c);
@@ -1659,6 +1973,7 @@ int mr_implicit_rhs(mr_ctx* c, double t, const double* y, double* out)
 int mr_slow_linear(mr_ctx* c, const double* A)
 {
   if (int g = pending_guard(c)) return g;
+  MR_FORWARD(c, mr_slow_linear(sl_, A));
   if (!c || !A || !c->has_grid || c->ncomp > MR_MAXLIN)
     return set_err(c, MR_CONTRACT, "mr_slow_linear: needs grid with n_comp <= 8");
   c->imex = false;
@@ -1672,6 +1987,7 @@ int mr_slow_none(mr_ctx* c)
 {
   if (!c) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  MR_FORWARD(c, mr_slow_none(sl_));
   c->slow_kind = SK_NONE;
   c->imex = false;
   return MR_OK;
@@ -1681,6 +1997,18 @@ int mr_state_upload(mr_ctx* c, const double* host)
 {
   if (!c || !host) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  if (!c->slabs.empty()) {
+    if (!c->has_grid) return set_err(c, MR_CONTRACT, "grid not set (mr_grid_set)");
+    std::vector<double*> bufs;
+    for (mr_ctx* sl : c->slabs) {
+      cudaSetDevice(sl->device);
+      if (int rc = ensure_state(sl)) return set_err(c, rc, sl->err);
+      bufs.push_back(sl->y_state);
+    }
+    const int rc = domain_copy(c, host, nullptr, bufs.data(), true);
+    for (mr_ctx* sl : c->slabs) sl->state_valid = rc == MR_OK;
+    return rc;
+  }
   cudaSetDevice(c->device);
   int rc = ensure_state(c);
   if (rc) return rc;
@@ -1695,6 +2023,14 @@ int mr_state_download(mr_ctx* c, double* host)
 {
   if (!c || !host) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  if (!c->slabs.empty()) {
+    std::vector<double*> bufs;
+    for (mr_ctx* sl : c->slabs) {
+      if (!sl->y_state) return set_err(c, MR_CONTRACT, "no state");
+      bufs.push_back(sl->y_state);
+    }
+    return domain_copy(c, nullptr, host, bufs.data(), false);
+  }
   if (!c->y_state) return set_err(c, MR_CONTRACT, "no state");
   cudaSetDevice(c->device);
   MR_CUDA_TRY(c, cudaMemcpyAsync(host, c->y_state, c->dof * sizeof(double),
@@ -1707,7 +2043,12 @@ int mr_state_download(mr_ctx* c, double* host)
 // (the commit is a host-side buffer swap): no pointer while one is pending
 double* mr_state_device_ptr(mr_ctx* c)
 {
-  if (!c || pending_guard(c) || ensure_state(c)) return nullptr;
+  if (!c || pending_guard(c)) return nullptr;
+  if (!c->slabs.empty()) {  // one buffer per GPU: no single pointer
+    set_err(c, MR_CONTRACT, "mr_state_device_ptr: not available on a multi-device domain");
+    return nullptr;
+  }
+  if (ensure_state(c)) return nullptr;
   return c->y_state;
 }
 
@@ -1717,6 +2058,9 @@ int mr_mri_step(mr_ctx* c, double t, double H, uint64_t* counters, int* fail_sta
 {
   if (!c) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  if (!c->slabs.empty())
+    return domain_rc(c, domain_step(c->slabs.data(), (int)c->slabs.size(), t, H, counters,
+                                    fail_stage));
   cudaSetDevice(c->device);
   mr_ctx* cs[1] = {c};
   return domain_step(cs, 1, t, H, counters, fail_stage);
@@ -1726,6 +2070,7 @@ int mr_mri_step_async(mr_ctx* c, double t, double H, void* stream)
 {
   if (!c) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  MR_NOT_ON_DOMAIN(c, "mr_mri_step_async");
   cudaSetDevice(c->device);
   if (!c->ev_async_in) {
     MR_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_async_in, cudaEventDisableTiming));
@@ -1774,34 +2119,39 @@ int mr_mri_integrate(mr_ctx* c, double t0, double tf, double H, uint64_t* counte
   if (int g = pending_guard(c)) return g;
   if (fail_stage) *fail_stage = -1;
   if (!(tf > t0)) return set_err(c, MR_CONTRACT, "mri_integrate: tf must exceed t0");
-  cudaSetDevice(c->device);
-  int rc = ensure_state(c);
-  if (rc) return rc;
-  const long n_steps = static_cast<long>(std::ceil((tf - t0) / H - 1e-12));
-  double* backup = nullptr;
-  if (n_steps > 1) {  // allocated once per grid, reused by every integrate call
-    if (!c->y_backup) MR_CUDA_TRY(c, cudaMalloc(&c->y_backup, c->dof * sizeof(double)));
-    backup = c->y_backup;
-    MR_CUDA_TRY(c, cudaMemcpyAsync(backup, c->y_state, c->dof * sizeof(double),
-                                   cudaMemcpyDeviceToDevice, c->stream));
+  const std::vector<mr_ctx*> ms = members(c);
+  for (mr_ctx* m : ms) {
+    cudaSetDevice(m->device);
+    if (int rc = ensure_state(m)) return set_err(c, rc, m->err);
   }
+  const long n_steps = static_cast<long>(std::ceil((tf - t0) / H - 1e-12));
+  const bool backup = n_steps > 1;
+  if (backup)  // allocated once per grid, reused by every integrate call
+    for (mr_ctx* m : ms) {
+      cudaSetDevice(m->device);
+      if (!m->y_backup) MR_CUDA_TRY(c, cudaMalloc(&m->y_backup, m->dof * sizeof(double)));
+      MR_CUDA_TRY(c, cudaMemcpyAsync(m->y_backup, m->y_state, m->dof * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, m->stream));
+    }
   double t = t0;
+  int rc = MR_OK;
   for (long i = 0; i < n_steps; ++i) {
     const double step = (i == n_steps - 1) ? (tf - t) : H;
     rc = mr_mri_step(c, t, step, counters, fail_stage);
     if (rc) break;
     t = (i == n_steps - 1) ? tf : t0 + static_cast<double>(i + 1) * H;
   }
-  if (backup) {
-    if (rc)
-      cudaMemcpyAsync(c->y_state, backup, c->dof * sizeof(double), cudaMemcpyDeviceToDevice,
-                      c->stream);
-    cudaStreamSynchronize(c->stream);
-  }
+  if (backup)
+    for (mr_ctx* m : ms) {
+      cudaSetDevice(m->device);
+      if (rc)
+        cudaMemcpyAsync(m->y_state, m->y_backup, m->dof * sizeof(double), cudaMemcpyDeviceToDevice,
+                        m->stream);
+      cudaStreamSynchronize(m->stream);
+    }
   return rc;
 }
 
-static int eval_fast_dev(mr_ctx* c, const double* in, double* out);
 
 // ---------------------------------------------------------------------------
 // ARK-IMEX: ark_imex_step (mri.cpp:437-522) with the
@@ -1847,7 +2197,8 @@ int ark_explicit(mr_ctx** cs, int n, double* const* in, double* const* out, cuda
 {
   const bool fast = cs[0]->fast_kind != FK_NONE, slow = cs[0]->slow_kind != SK_NONE;
   for (int r = 0; r < n && fast; ++r) {
-    int rc = eval_fast_dev(cs[r], in[r], cs[r]->ark_bufs[12]);
+    sdev(cs[r]);
+    int rc = eval_fast_dev(cs[r], in[r], cs[r]->ark_bufs[12], sst(cs[r], st));
     if (rc) return rc;
   }
   if (slow) {
@@ -1856,8 +2207,9 @@ int ark_explicit(mr_ctx** cs, int n, double* const* in, double* const* out, cuda
     if (rc) return rc;
   }
   for (int r = 0; r < n; ++r) {
+    sdev(cs[r]);
     MR_CUDA_TRY(cs[r], launch_add2(cs[r]->dof, fast ? cs[r]->ark_bufs[12] : nullptr,
-                                   slow ? out[r] : nullptr, out[r], st));
+                                   slow ? out[r] : nullptr, out[r], sst(cs[r], st)));
     cs[r]->launches++;
   }
   return MR_OK;
@@ -1870,6 +2222,7 @@ int ark_domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, 
   if (!(H > 0.0)) return set_err(c0, MR_CONTRACT, "ark_imex_step: H must be positive");
   for (int r = 0; r < n; ++r) {
     mr_ctx* c = cs[r];
+    sdev(c);
     if (!c->has_grid) return set_err(c0, MR_CONTRACT, "grid not set (mr_grid_set)");
     if (c->fast_kind < 0 || c->slow_kind < 0)
       return set_err(c0, MR_CONTRACT, "PartitionedSystem: fast/slow plugins not configured");
@@ -1884,7 +2237,7 @@ int ark_domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, 
       MR_CUDA_TRY(c, cudaMalloc(&p, c->dof * sizeof(double)));
       c->ark_bufs.push_back(p);
     }
-    MR_CUDA_TRY(c, cudaMemsetAsync(c->d_fail, 0xFF, sizeof(unsigned long long), c0->stream));
+    MR_CUDA_TRY(c, cudaMemsetAsync(c->d_fail, 0xFF, sizeof(unsigned long long), sst(c, c0->stream)));
   }
   static const Ark436 tb;
   const int s = 6;
@@ -1915,6 +2268,7 @@ int ark_domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, 
     // known = y + sum_j H (AE_ij fE_j, then AI_ij fI_j)   (mri.cpp:467-471)
     for (int r = 0; r < n; ++r) {
       mr_ctx* c = cs[r];
+      sdev(c);
       const double* f[MR_MAXREF];
       double cf[MR_MAXREF];
       int nref = 0;
@@ -1922,9 +2276,10 @@ int ark_domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, 
         if (tb.AE[i][j] != 0.0) { f[nref] = c->ark_bufs[j]; cf[nref++] = H * tb.AE[i][j]; }
         if (tb.AI[i][j] != 0.0) { f[nref] = c->ark_bufs[6 + j]; cf[nref++] = H * tb.AI[i][j]; }
       }
-      MR_CUDA_TRY(c, launch_update(c->y_state, c->cg_known, nref, f, cf, c->dof, i, c->d_fail, st));
+      MR_CUDA_TRY(c, launch_update(c->y_state, c->cg_known, nref, f, cf, c->dof, i, c->d_fail,
+                                   sst(c, st)));
       MR_CUDA_TRY(c, cudaMemcpyAsync(c->y_work, c->cg_known, c->dof * sizeof(double),
-                                     cudaMemcpyDeviceToDevice, st));
+                                     cudaMemcpyDeviceToDevice, sst(c, st)));
       c->launches++;
       out[r] = c->ark_bufs[6 + i];
     }
@@ -1950,6 +2305,7 @@ int ark_domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, 
     // out = y + sum_j H b_j (fE_j, then fI_j)   (mri.cpp:510-516)
     for (int r = 0; r < n; ++r) {
       mr_ctx* c = cs[r];
+      sdev(c);
       const double* f[MR_MAXREF];
       double cf[MR_MAXREF];
       int nref = 0;
@@ -1958,17 +2314,24 @@ int ark_domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, 
           f[nref] = c->ark_bufs[j]; cf[nref++] = H * tb.b[j];
           f[nref] = c->ark_bufs[6 + j]; cf[nref++] = H * tb.b[j];
         }
-      MR_CUDA_TRY(c, launch_update(c->y_state, c->y_work, nref, f, cf, c->dof, s, c->d_fail, st));
+      MR_CUDA_TRY(c, launch_update(c->y_state, c->y_work, nref, f, cf, c->dof, s, c->d_fail,
+                                   sst(c, st)));
       c->launches++;
     }
   }
   unsigned long long key = MR_NO_FAIL;
   if (n == 1 && c0->comm)
     MR_NCCL_TRY(c0, AllReduce(c0->d_fail, c0->d_fail, 1, ncclUint64, ncclMin, c0->comm, st));
-  for (int r = 0; r < n; ++r)
+  for (int r = 0; r < n; ++r) {
+    sdev(cs[r]);
     MR_CUDA_TRY(cs[r], cudaMemcpyAsync(cs[r]->h_fail, cs[r]->d_fail, sizeof(unsigned long long),
-                                       cudaMemcpyDeviceToHost, st));
-  MR_CUDA_TRY(c0, cudaStreamSynchronize(st));
+                                       cudaMemcpyDeviceToHost, sst(cs[r], st)));
+  }
+  for (int r = 0; r < n; ++r) {
+    if (!cs[r]->in_domain && r > 0) break;
+    sdev(cs[r]);
+    MR_CUDA_TRY(c0, cudaStreamSynchronize(sst(cs[r], st)));
+  }
   for (int r = 0; r < n; ++r) key = std::min(key, *cs[r]->h_fail);
   key = std::min(key, host_key);
   if (key != MR_NO_FAIL) {
@@ -1995,6 +2358,9 @@ int mr_ark_imex_step(mr_ctx* c, double t, double H, uint64_t* counters, int* fai
 {
   if (!c) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  if (!c->slabs.empty())
+    return domain_rc(c, ark_domain_step(c->slabs.data(), (int)c->slabs.size(), t, H, counters,
+                                        fail_stage));
   cudaSetDevice(c->device);
   return ark_domain_step(&c, 1, t, H, counters, fail_stage);
 }
@@ -2006,30 +2372,36 @@ int mr_ark_imex_integrate(mr_ctx* c, double t0, double tf, double H, uint64_t* c
   if (int g = pending_guard(c)) return g;
   if (fail_stage) *fail_stage = -1;
   if (!(tf > t0)) return set_err(c, MR_CONTRACT, "ark_imex_integrate: tf must exceed t0");
-  cudaSetDevice(c->device);
-  int rc = ensure_state(c);
-  if (rc) return rc;
-  const long n_steps = static_cast<long>(std::ceil((tf - t0) / H - 1e-12));
-  double* backup = nullptr;
-  if (n_steps > 1) {  // allocated once per grid, reused by every integrate call
-    if (!c->y_backup) MR_CUDA_TRY(c, cudaMalloc(&c->y_backup, c->dof * sizeof(double)));
-    backup = c->y_backup;
-    MR_CUDA_TRY(c, cudaMemcpyAsync(backup, c->y_state, c->dof * sizeof(double),
-                                   cudaMemcpyDeviceToDevice, c->stream));
+  const std::vector<mr_ctx*> ms = members(c);
+  for (mr_ctx* m : ms) {
+    cudaSetDevice(m->device);
+    if (int rc = ensure_state(m)) return set_err(c, rc, m->err);
   }
+  const long n_steps = static_cast<long>(std::ceil((tf - t0) / H - 1e-12));
+  const bool backup = n_steps > 1;
+  if (backup)
+    for (mr_ctx* m : ms) {
+      cudaSetDevice(m->device);
+      if (!m->y_backup) MR_CUDA_TRY(c, cudaMalloc(&m->y_backup, m->dof * sizeof(double)));
+      MR_CUDA_TRY(c, cudaMemcpyAsync(m->y_backup, m->y_state, m->dof * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, m->stream));
+    }
   double t = t0;
+  int rc = MR_OK;
   for (long i = 0; i < n_steps; ++i) {
     const double step = (i == n_steps - 1) ? (tf - t) : H;
-    rc = ark_domain_step(&c, 1, t, step, counters, fail_stage);
+    rc = mr_ark_imex_step(c, t, step, counters, fail_stage);
     if (rc) break;
     t = (i == n_steps - 1) ? tf : t0 + static_cast<double>(i + 1) * H;
   }
-  if (backup) {
-    if (rc)
-      cudaMemcpyAsync(c->y_state, backup, c->dof * sizeof(double), cudaMemcpyDeviceToDevice,
-                      c->stream);
-    cudaStreamSynchronize(c->stream);
-  }
+  if (backup)
+    for (mr_ctx* m : ms) {
+      cudaSetDevice(m->device);
+      if (rc)
+        cudaMemcpyAsync(m->y_state, m->y_backup, m->dof * sizeof(double), cudaMemcpyDeviceToDevice,
+                        m->stream);
+      cudaStreamSynchronize(m->stream);
+    }
   return rc;
 }
 
@@ -2038,6 +2410,13 @@ int mr_mri_step_host(mr_ctx* c, double t, double H, const double* y_in, double* 
 {
   if (!c || !y_in || !y_out) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  if (!c->slabs.empty()) {
+    int rc = mr_state_upload(c, y_in);
+    if (rc) return rc;
+    rc = mr_mri_step(c, t, H, counters, fail_stage);
+    if (rc) return rc;
+    return mr_state_download(c, y_out);
+  }
   cudaSetDevice(c->device);
   int rc = ensure_state(c);
   if (rc) return rc;
@@ -2054,6 +2433,7 @@ int mr_mri_step_host(mr_ctx* c, double t, double H, const double* y_in, double* 
 int mr_last_failure(const mr_ctx* c, int* mri_stage, int* substep, int* inner_stage)
 {
   if (!c) return MR_CONTRACT;
+  if (!c->slabs.empty()) c = c->slabs[0];
   if (mri_stage) *mri_stage = c->fail_mri;
   if (substep) *substep = c->fail_sub;
   if (inner_stage) *inner_stage = c->fail_inner;
@@ -2072,6 +2452,11 @@ int mr_fast_rhs(mr_ctx* c, double t, const double* y, double* out)
   (void)t;
   if (!c || !y || !out) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  if (!c->slabs.empty()) {
+    if (!c->has_grid || c->slabs[0]->fast_kind < 0)
+      return set_err(c, MR_CONTRACT, "fast plugin not set");
+    return domain_rhs(c, 0, y, out);
+  }
   if (!c->has_grid || c->fast_kind < 0) return set_err(c, MR_CONTRACT, "fast plugin not set");
   if (c->fast_kind == FK_CHEM && c->ncomp != c->S + 1)
     return set_err(c, MR_CONTRACT, "chemistry plugin needs n_comp == S + 1");
@@ -2102,136 +2487,145 @@ int mr_fast_rhs(mr_ctx* c, double t, const double* y, double* out)
   return MR_OK;
 }
 
-// one fast-partition RHS evaluation between device buffers
-static int eval_fast_dev(mr_ctx* c, const double* in, double* out)
-{
-  if (c->fast_kind == FK_CHEM) {
-    ChemCfg ccfg;
-    TableDev t4{};
-    t4.s = 4;
-    if (chem_pick(&ccfg, c->ncomp, c->S, c->R, t4, 1))
-      return set_err(c, MR_CONTRACT, "unsupported mechanism size");
-    MR_CUDA_TRY(c, launch_chem_rhs(ccfg, in, out, c->ncell, c->ncomp, *c->chemP, c->stream));
-  } else {
-    ChainCfg cfg;
-    if (chain_pick(&cfg, c->fast_kind, c->ncomp, 4, 1))
-      return set_err(c, MR_CONTRACT, "unsupported component count");
-    MR_CUDA_TRY(c, launch_fast_rhs(cfg, in, out, c->ncell, c->ncomp, c->fastA, c->stream));
-  }
-  c->launches++;
-  return MR_OK;
-}
+
 
 // erk_integrate (erk.cpp:40-57) of an explicit table on sum_rhs
 // (partitioned_system.hpp:41-48) over the device-resident state: erk_step's
 // stage loop, finite checks (:24-36) and per-stage evaluation count (:28).
 // On failure the state is restored to its value at entry (the reference's
 // input is const) and the count stops where erk_step threw.
-static int erk_integrate_dev(mr_ctx* c, int s, const double* A, const double* b, double t0,
-                             double tf, double h, uint64_t* evals, int* fail_stage)
+static int erk_integrate_dev(mr_ctx** cs, int n, int s, const double* A, const double* b,
+                             double t0, double tf, double h, uint64_t* evals, int* fail_stage)
 {
   if (fail_stage) *fail_stage = -1;
-  if (!c) return MR_CONTRACT;
-  if (!c->has_grid) return set_err(c, MR_CONTRACT, "grid not set (mr_grid_set)");
-  if (c->fast_kind < 0 || c->slow_kind < 0)
-    return set_err(c, MR_CONTRACT, "PartitionedSystem: fast/slow plugins not configured");
-  if (c->fast_kind == FK_NONE && c->slow_kind == SK_NONE)
-    return set_err(c, MR_CONTRACT, "PartitionedSystem: at least one partition required");
-  if (!(tf > t0)) return set_err(c, MR_CONTRACT, "erk_integrate: tf must exceed t0");
-  if (!(h > 0.0)) return set_err(c, MR_CONTRACT, "erk_integrate: h must be positive");
-  if (s < 1 || s > MR_MAXREF) return set_err(c, MR_CONTRACT, "erk_integrate: 1 <= stages <= 12");
+  mr_ctx* c0 = cs[0];
+  if (!c0->has_grid) return set_err(c0, MR_CONTRACT, "grid not set (mr_grid_set)");
+  if (c0->fast_kind < 0 || c0->slow_kind < 0)
+    return set_err(c0, MR_CONTRACT, "PartitionedSystem: fast/slow plugins not configured");
+  if (c0->fast_kind == FK_NONE && c0->slow_kind == SK_NONE)
+    return set_err(c0, MR_CONTRACT, "PartitionedSystem: at least one partition required");
+  if (!(tf > t0)) return set_err(c0, MR_CONTRACT, "erk_integrate: tf must exceed t0");
+  if (!(h > 0.0)) return set_err(c0, MR_CONTRACT, "erk_integrate: h must be positive");
+  if (s < 1 || s > MR_MAXREF) return set_err(c0, MR_CONTRACT, "erk_integrate: 1 <= stages <= 12");
   for (int i = 0; i < s; ++i)
     for (int j = i; j < s; ++j)
-      if (A[i * s + j] != 0.0) return set_err(c, MR_CONTRACT, "erk_step: table must be explicit");
-  if (c->slow_kind == SK_STENCIL && c->n0l < c->M)
-    return set_err(c, MR_CONTRACT, "slab thinner than the stencil ghost width");
-  cudaSetDevice(c->device);
-  int rc = ensure_state(c);
-  if (rc) return rc;
-  // buffers: k[0..s-1], stage, f_fast, f_implicit, entry backup
-  while ((int)c->rs_bufs.size() < s + 4) {
-    double* p = nullptr;
-    MR_CUDA_TRY(c, cudaMalloc(&p, c->dof * sizeof(double)));
-    c->rs_bufs.push_back(p);
+      if (A[i * s + j] != 0.0) return set_err(c0, MR_CONTRACT, "erk_step: table must be explicit");
+  for (int r = 0; r < n; ++r) {
+    mr_ctx* c = cs[r];
+    if (c->slow_kind == SK_STENCIL && c->n0l < c->M)
+      return set_err(c0, MR_CONTRACT, "slab thinner than the stencil ghost width");
+    cudaSetDevice(c->device);
+    int rc = ensure_state(c);
+    if (rc) return rc;
+    // buffers: k[0..s-1], stage, f_fast, f_implicit, entry backup
+    while ((int)c->rs_bufs.size() < s + 4) {
+      double* p = nullptr;
+      MR_CUDA_TRY(c, cudaMalloc(&p, c->dof * sizeof(double)));
+      c->rs_bufs.push_back(p);
+    }
   }
-  double** k = c->rs_bufs.data();
-  double* stage = c->rs_bufs[s];
-  double* tf_ = c->rs_bufs[s + 1];
-  double* ti_ = c->rs_bufs[s + 2];
-  double* backup = c->rs_bufs[s + 3];
-  const bool fast = c->fast_kind != FK_NONE, slow = c->slow_kind != SK_NONE;
-  const bool imp = c->slow_kind == SK_STENCIL && c->imex;
-  cudaStream_t st = c->stream;
-  MR_CUDA_TRY(c, cudaMemcpyAsync(backup, c->y_state, c->dof * sizeof(double),
-                                 cudaMemcpyDeviceToDevice, st));
+  const bool fast = c0->fast_kind != FK_NONE, slow = c0->slow_kind != SK_NONE;
+  const bool imp = c0->slow_kind == SK_STENCIL && c0->imex;
+  cudaStream_t st = c0->stream;
+  auto buf = [&](int r, int q) { return cs[r]->rs_bufs[q]; };  // k_q (q < s), stage, f_F, f_I, backup
+  for (int r = 0; r < n; ++r) {
+    sdev(cs[r]);
+    MR_CUDA_TRY(cs[r], cudaMemcpyAsync(buf(r, s + 3), cs[r]->y_state, cs[r]->dof * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, sst(cs[r], st)));
+  }
+  std::vector<const double*> yc(n);
+  std::vector<double*> oc(n);
   const long n_steps = (long)std::ceil((tf - t0) / h - 1e-12);
   double t = t0;
-  for (long n = 0; n < n_steps; ++n) {
-    const double step = (n == n_steps - 1) ? (tf - t) : h;
-    MR_CUDA_TRY(c, cudaMemsetAsync(c->d_fail, 0xFF, sizeof(unsigned long long), st));
+  for (long ns = 0; ns < n_steps; ++ns) {
+    const double step = (ns == n_steps - 1) ? (tf - t) : h;
+    for (int r = 0; r < n; ++r) {
+      sdev(cs[r]);
+      MR_CUDA_TRY(cs[r], cudaMemsetAsync(cs[r]->d_fail, 0xFF, sizeof(unsigned long long),
+                                         sst(cs[r], st)));
+    }
     for (int i = 0; i < s; ++i) {
-      const double* f[MR_MAXREF];
-      double cf[MR_MAXREF];
-      int nref = 0;
-      for (int j = 0; j < i; ++j)
-        if (A[i * s + j] != 0.0) {
-          f[nref] = k[j];
-          cf[nref++] = step * A[i * s + j];
+      for (int r = 0; r < n; ++r) {
+        mr_ctx* c = cs[r];
+        sdev(c);
+        const double* f[MR_MAXREF];
+        double cf[MR_MAXREF];
+        int nref = 0;
+        for (int j = 0; j < i; ++j)
+          if (A[i * s + j] != 0.0) {
+            f[nref] = buf(r, j);
+            cf[nref++] = step * A[i * s + j];
+          }
+        MR_CUDA_TRY(c, launch_update(c->y_state, buf(r, s), nref, f, cf, c->dof, i, c->d_fail,
+                                     sst(c, st)));
+        c->launches++;
+        if (fast) {
+          int rc = eval_fast_dev(c, buf(r, s), buf(r, s + 1), sst(c, st));
+          if (rc) return rc;
         }
-      MR_CUDA_TRY(c, launch_update(c->y_state, stage, nref, f, cf, c->dof, i, c->d_fail, st));
-      c->launches++;
-      if (fast) {
-        rc = eval_fast_dev(c, stage, tf_);
-        if (rc) return rc;
       }
+      for (int r = 0; r < n; ++r) yc[r] = buf(r, s);
       if (imp) {
-        mr_ctx* cs[1] = {c};
-        const double* yc[1] = {stage};
-        double* oc[1] = {ti_};
-        rc = eval_implicit(cs, 1, yc, oc, st);
+        for (int r = 0; r < n; ++r) oc[r] = buf(r, s + 2);
+        int rc = eval_implicit(cs, n, yc.data(), oc.data(), st);
         if (rc) return rc;
       }
       if (slow) {
-        mr_ctx* cs[1] = {c};
-        const double* yc[1] = {stage};
-        double* oc[1] = {k[i]};
-        rc = eval_slow(cs, 1, yc, oc, st);
+        for (int r = 0; r < n; ++r) oc[r] = buf(r, i);
+        int rc = eval_slow(cs, n, yc.data(), oc.data(), st);
         if (rc) return rc;
       }
-      MR_CUDA_TRY(c, launch_sum_rhs(c->dof, fast ? tf_ : nullptr, imp ? ti_ : nullptr,
-                                    slow ? k[i] : nullptr, k[i], st));
-      c->launches++;
+      for (int r = 0; r < n; ++r) {
+        mr_ctx* c = cs[r];
+        sdev(c);
+        MR_CUDA_TRY(c, launch_sum_rhs(c->dof, fast ? buf(r, s + 1) : nullptr,
+                                      imp ? buf(r, s + 2) : nullptr, slow ? buf(r, i) : nullptr,
+                                      buf(r, i), sst(c, st)));
+        c->launches++;
+      }
     }
-    {
+    for (int r = 0; r < n; ++r) {
+      mr_ctx* c = cs[r];
+      sdev(c);
       const double* f[MR_MAXREF];
       double cf[MR_MAXREF];
       int nref = 0;
       for (int i = 0; i < s; ++i)
         if (b[i] != 0.0) {
-          f[nref] = k[i];
+          f[nref] = buf(r, i);
           cf[nref++] = step * b[i];
         }
-      MR_CUDA_TRY(c, launch_update(c->y_state, c->y_work, nref, f, cf, c->dof, s, c->d_fail, st));
+      MR_CUDA_TRY(c, launch_update(c->y_state, c->y_work, nref, f, cf, c->dof, s, c->d_fail,
+                                   sst(c, st)));
       c->launches++;
+      if (c->comm)
+        MR_NCCL_TRY(c, AllReduce(c->d_fail, c->d_fail, 1, ncclUint64, ncclMin, c->comm, sst(c, st)));
+      MR_CUDA_TRY(c, cudaMemcpyAsync(c->h_fail, c->d_fail, sizeof(unsigned long long),
+                                     cudaMemcpyDeviceToHost, sst(c, st)));
     }
-    if (c->comm)
-      MR_NCCL_TRY(c, AllReduce(c->d_fail, c->d_fail, 1, ncclUint64, ncclMin, c->comm, st));
-    MR_CUDA_TRY(c, cudaMemcpyAsync(c->h_fail, c->d_fail, sizeof(unsigned long long),
-                                   cudaMemcpyDeviceToHost, st));
-    MR_CUDA_TRY(c, cudaStreamSynchronize(st));
-    if (*c->h_fail != MR_NO_FAIL) {
-      const int fs = (int)(*c->h_fail >> 40);
+    unsigned long long key = MR_NO_FAIL;
+    for (int r = 0; r < n; ++r) {
+      sdev(cs[r]);
+      MR_CUDA_TRY(cs[r], cudaStreamSynchronize(sst(cs[r], st)));
+      key = std::min(key, *cs[r]->h_fail);
+    }
+    if (key != MR_NO_FAIL) {
+      const int fs = (int)(key >> 40);
       if (fail_stage) *fail_stage = fs;
       if (evals) *evals += (uint64_t)(fs < s ? fs : s);  // stages evaluated before the throw
-      MR_CUDA_TRY(c, cudaMemcpyAsync(c->y_state, backup, c->dof * sizeof(double),
-                                     cudaMemcpyDeviceToDevice, st));
-      MR_CUDA_TRY(c, cudaStreamSynchronize(st));
-      return set_err(c, MR_INTEGRATION,
+      for (int r = 0; r < n; ++r) {
+        sdev(cs[r]);
+        MR_CUDA_TRY(cs[r], cudaMemcpyAsync(cs[r]->y_state, buf(r, s + 3),
+                                           cs[r]->dof * sizeof(double), cudaMemcpyDeviceToDevice,
+                                           sst(cs[r], st)));
+        MR_CUDA_TRY(cs[r], cudaStreamSynchronize(sst(cs[r], st)));
+      }
+      return set_err(c0, MR_INTEGRATION,
                      fs == s ? "erk_step: non-finite result" : "erk_step: non-finite stage value");
     }
     if (evals) *evals += (uint64_t)s;
-    std::swap(c->y_state, c->y_work);
-    t = (n == n_steps - 1) ? tf : t0 + (double)(n + 1) * h;
+    for (int r = 0; r < n; ++r) std::swap(cs[r]->y_state, cs[r]->y_work);
+    t = (ns == n_steps - 1) ? tf : t0 + (double)(ns + 1) * h;
   }
   return MR_OK;
 }
@@ -2242,7 +2636,10 @@ int mr_erk_integrate(mr_ctx* c, int s, const double* A, const double* b, const d
   (void)cvec;  // sum_rhs of the plugins is autonomous: t + c_i h is not consumed
   if (!c || !A || !b) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
-  return erk_integrate_dev(c, s, A, b, t0, tf, h, n_explicit_evals, fail_stage);
+  if (!c->slabs.empty())
+    return domain_rc(c, erk_integrate_dev(c->slabs.data(), (int)c->slabs.size(), s, A, b, t0, tf,
+                                          h, n_explicit_evals, fail_stage));
+  return erk_integrate_dev(&c, 1, s, A, b, t0, tf, h, n_explicit_evals, fail_stage);
 }
 
 // reference_solution (erk.cpp:59-75): erk_integrate of cash-karp5
@@ -2259,7 +2656,10 @@ int mr_reference_solution(mr_ctx* c, double t0, double tf, double h, int* fail_s
   A[5][0] = 1631.0 / 55296.0; A[5][1] = 175.0 / 512.0; A[5][2] = 575.0 / 13824.0;
   A[5][3] = 44275.0 / 110592.0; A[5][4] = 253.0 / 4096.0;
   b[0] = 37.0 / 378.0; b[2] = 250.0 / 621.0; b[3] = 125.0 / 594.0; b[5] = 512.0 / 1771.0;
-  return erk_integrate_dev(c, 6, &A[0][0], b, t0, tf, h, nullptr, fail_stage);
+  if (!c->slabs.empty())
+    return domain_rc(c, erk_integrate_dev(c->slabs.data(), (int)c->slabs.size(), 6, &A[0][0], b,
+                                          t0, tf, h, nullptr, fail_stage));
+  return erk_integrate_dev(&c, 1, 6, &A[0][0], b, t0, tf, h, nullptr, fail_stage);
 }
 
 int mr_slow_rhs(mr_ctx* c, double t, const double* y, double* out)
@@ -2267,6 +2667,18 @@ int mr_slow_rhs(mr_ctx* c, double t, const double* y, double* out)
   (void)t;
   if (!c || !y || !out) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  if (!c->slabs.empty()) {
+    if (!c->has_grid || c->slabs[0]->slow_kind < 0)
+      return set_err(c, MR_CONTRACT, "slow plugin not set");
+    if (c->slabs[0]->slow_kind == SK_NONE) {
+      std::memset(out, 0, c->dof * sizeof(double));
+      return MR_OK;
+    }
+    for (mr_ctx* sl : c->slabs)
+      if (sl->slow_kind == SK_STENCIL && sl->n0l < sl->M)
+        return set_err(c, MR_CONTRACT, "slab thinner than the stencil ghost width");
+    return domain_rhs(c, 1, y, out);
+  }
   if (!c->has_grid || c->slow_kind < 0) return set_err(c, MR_CONTRACT, "slow plugin not set");
   if (c->slow_kind == SK_STENCIL && c->n0l < c->M)
     return set_err(c, MR_CONTRACT, "slab thinner than the stencil ghost width");
@@ -2295,6 +2707,7 @@ static int reduce(mr_ctx* c, int kind, const double* x, const double* w, size_t 
 {
   if (!c || !x || !out) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  MR_NOT_ON_DOMAIN(c, "device-pointer reductions");
   cudaSetDevice(c->device);
   const int nb = reduce_blocks();
   double* part = c->d_red;
@@ -2377,6 +2790,7 @@ int mr_comm_init(mr_ctx* c, int nranks, int rank, const char* id128)
 {
   if (!c || nranks < 1 || rank < 0 || rank >= nranks || !id128) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  MR_NOT_ON_DOMAIN(c, "mr_comm_init");
   if (c->comm) return set_err(c, MR_CONTRACT, "mr_comm_init: communicator already set");
   cudaSetDevice(c->device);
   if (nranks == 1) {  // no communicator: the periodic single-slab path
@@ -2394,6 +2808,7 @@ int mr_comm_init_loopback(mr_ctx* c)
 {
   if (!c) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  MR_NOT_ON_DOMAIN(c, "mr_comm_init_loopback");
   if (c->comm) return set_err(c, MR_CONTRACT, "mr_comm_init_loopback: communicator already set");
   cudaSetDevice(c->device);
   ncclUniqueId id;
@@ -2406,7 +2821,8 @@ int mr_group_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, in
 {
   if (!cs || n < 1) return MR_CONTRACT;
   for (int r = 0; r < n; ++r) {
-    if (!cs[r] || cs[r]->device != cs[0]->device || cs[r]->nranks != 1 || cs[r]->comm)
+    if (!cs[r] || cs[r]->device != cs[0]->device || cs[r]->nranks != 1 || cs[r]->comm ||
+        !cs[r]->slabs.empty() || cs[r]->in_domain)
       return set_err(cs[0], MR_CONTRACT, "mr_group_step: contexts must share one device");
     if (cs[r]->pending.active)
       return set_err(cs[0], MR_CONTRACT, "an asynchronous step is in flight: call mr_mri_step_wait first");
@@ -2550,12 +2966,23 @@ int mr_debug_chem_phases(mr_ctx* c, uint64_t* out, int reset)
 }
 
 void* mr_stream(mr_ctx* c) { return c ? (void*)c->stream : nullptr; }
-uint64_t mr_launch_count(const mr_ctx* c) { return c ? c->launches : 0; }
-double mr_chem_flops_per_eval(const mr_ctx* c) { return c ? c->chem_flops : 0.0; }
+uint64_t mr_launch_count(const mr_ctx* c)
+{
+  if (!c) return 0;
+  uint64_t n = c->launches;
+  for (const mr_ctx* sl : c->slabs) n += sl->launches;
+  return n;
+}
+double mr_chem_flops_per_eval(const mr_ctx* c)
+{
+  if (c && !c->slabs.empty()) c = c->slabs[0];
+  return c ? c->chem_flops : 0.0;
+}
 
 int mr_fp64_peak(mr_ctx* c, double* tflops)
 {
   if (!c || !tflops) return MR_CONTRACT;
+  if (!c->slabs.empty()) c = c->slabs[0];
   cudaSetDevice(c->device);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -2584,6 +3011,7 @@ int mr_set_profiling(mr_ctx* c, int enable)
 {
   if (!c) return MR_CONTRACT;
   if (int g = pending_guard(c)) return g;
+  MR_FORWARD(c, mr_set_profiling(sl_, enable));
   c->profile = enable != 0;
   return MR_OK;
 }
@@ -2591,6 +3019,7 @@ int mr_set_profiling(mr_ctx* c, int enable)
 int mr_last_step_profile(const mr_ctx* c, double* chem_ms, double* slow_ms, double* other_ms)
 {
   if (!c) return MR_CONTRACT;
+  if (!c->slabs.empty()) c = c->slabs[0];
   if (chem_ms) *chem_ms = c->prof_chem;
   if (slow_ms) *slow_ms = c->prof_slow;
   if (other_ms) *other_ms = c->prof_other;
