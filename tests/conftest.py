@@ -24,11 +24,12 @@ def _built():
     import paper_2211_03293_b200 as P
     if not os.path.exists(P.LIB_PATH):
         P.build()
-    facade = os.path.join(os.path.dirname(oracle.LIB), "_ref", "libfacade_test.so")
-    if os.path.isdir(oracle.REF_SRC) and not os.path.exists(facade):
-        import subprocess
-        subprocess.run(["make", "-C", os.path.dirname(oracle.LIB), "facade"], check=True,
-                       stdout=subprocess.DEVNULL)
+    ref_dir = os.path.join(os.path.dirname(oracle.LIB), "_ref")
+    for target, out in (("facade", "libfacade_test.so"), ("harness", "libharness_test.so")):
+        if os.path.isdir(oracle.REF_SRC) and not os.path.exists(os.path.join(ref_dir, out)):
+            import subprocess
+            subprocess.run(["make", "-C", os.path.dirname(oracle.LIB), target], check=True,
+                           stdout=subprocess.DEVNULL)
     yield
 
 

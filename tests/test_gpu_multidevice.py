@@ -108,7 +108,7 @@ def test_domain_rhs_ark_and_reference_solution():
     assert np.array_equal(one.download(), dom.download())
     one.upload(y0)
     dom.upload(y0)
-    H = 1e-15
+    H = 1e-17  # the ARK explicit part carries the stiff chemistry
     c1 = one.ark_imex_step(0.0, H)
     c2 = dom.ark_imex_step(0.0, H)
     assert np.array_equal(c1[[0, 1, 2, 3, 7]], c2[[0, 1, 2, 3, 7]])

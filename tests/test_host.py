@@ -147,3 +147,23 @@ def test_coupling_texts_ship_with_package():
         gold = open(os.path.join(ROOT, "tests", "golden", "couplings", f"{name}.txt")).read()
         assert P.coupling_text(name) == gold
         P.coupling_inspect(name)
+
+
+def test_reference_harness_is_routed_unmodified():
+    """proj/src/harness.cpp compiled unmodified with the routing prefix of
+    include/multirate_b200_harness.hpp: run_method's integrator calls resolve
+    to the routing functions, which the test driver defines
+    and which fall back to the reference's own integrators."""
+    import subprocess
+    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    obj = os.path.join(ref_dir, "harness_routed.o")
+    lib = os.path.join(ref_dir, "libharness_test.so")
+    if not os.path.exists(obj):
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    und = subprocess.run(["nm", "-C", "-u", obj], capture_output=True, text=True).stdout
+    for f in ("mri_integrate_routed", "ark_imex_integrate_routed", "erk_integrate_routed"):
+        assert f"multirate::{f}(" in und
+    assert "multirate::mri_integrate(" not in und  # every call site routed
+    defs = subprocess.run(["nm", "-C", "--defined-only", lib], capture_output=True, text=True).stdout
+    for f in ("mri_integrate_routed", "run_method", "harness_selftest", "RunReport::write_csv"):
+        assert f in defs, f
