@@ -3,7 +3,13 @@
 Seeds are fixed here (BASELINE.json gives none), as the reference records its
 `seed` in summary.json (proj/src/harness.cpp:669-675).  H is chosen from the
 chemistry's stiffness by oracle/stiffness.py (h * lambda_max = 1 for the inner
-RK4 at t = 0) -- BASELINE.json does not state it.
+RK4 at t = 0) -- BASELINE.json does not state it -- and then checked on the
+GPU over the whole grid by step halving (scripts/hcheck.py: one step of H vs
+two of H/2 on the slabs through the hotspot, per-species max relative
+difference).  The sampled lambda_max missed the stiffest cells of C4 and C5:
+at 3.6e-15 / 6.7e-15 the hotspot cells differed by O(1) (C5 even overflowed),
+so their H was halved to 1.8e-15 / 3.3e-15 (differences 1.3e-6 / 3.1e-6;
+C1-C3: <= 1.5e-5 at their H).  A step's cost does not depend on H.
 
 Coupling stand-ins: "MRI-GARK-ERK33" -> the reference's
 registered ``mis-kw3``; "MRI-GARK-ERK45a" -> ``imex-mri-gark4-explicit``, the
@@ -26,11 +32,11 @@ CONFIGS = {
                fast_table="classic-rk4", m=50, steps=4, rho=1e-3, H=1.4e-15, ngpu=(1, 2, 4)),
     "C4": dict(n=256, S=53, R=325, mech_seed=20221105, ic_seed=4, vel_seed=44, velocity="random",
                u=None, order=8, diffusion=1e-3, coupling="imex-mri-gark4-explicit",
-               fast_table="classic-rk4", m=50, steps=4, rho=1e-3, H=3.6e-15, ngpu=(1, 2, 4, 8)),
+               fast_table="classic-rk4", m=50, steps=4, rho=1e-3, H=1.8e-15, ngpu=(1, 2, 4, 8)),
     "C5": dict(n=384, S=53, R=325, mech_seed=20221105, ic_seed=5, vel_seed=55, velocity="random",
                u=None, order=8, diffusion=0.0, d_impl=5e-3, cg_iters=4,
                coupling="imex-mri-gark3b", fast_table="kutta3", m=100, steps=4, rho=1e-3,
-               H=6.7e-15, ngpu=(8,)),
+               H=3.3e-15, ngpu=(8,)),
 }
 
 
