@@ -88,8 +88,6 @@ struct ChemParams {
 
 struct ChemCfg {
   int NW, SPL;  // warps per block (slots), components per thread
-  int cpt;      // cells per thread: 1 (kernels_chem.cuh, 32 cells per block) or
-                // 2 (kernels_chem2.cuh, 64 cells per block)
   bool subdiag;
   int nstage;  // inner table stages (non-subdiagonal tables: stage accumulators)
   int ndeg;

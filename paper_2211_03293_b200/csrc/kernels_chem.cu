@@ -4,7 +4,6 @@
 #include <cuda_runtime.h>
 
 #include "kernels_chem.cuh"
-#include "kernels_chem2.cuh"
 
 namespace mrchem {
 #define MR_DECL(A, B)                                                                      \
@@ -19,16 +18,6 @@ MR_DECL(32, 2)
 #undef MR_DECL
 extern template cudaError_t run_chem_chain<32, 2, false, 3, 1>(const ChainArgs&, const ChemParams&, cudaStream_t);
 extern template cudaError_t run_chem_chain<32, 2, false, 3, 2>(const ChainArgs&, const ChemParams&, cudaStream_t);
-#define MR_DECL2(A, B)                                                                      \
-  extern template cudaError_t run_chem2_chain<A, B, true, 4, 1>(const ChainArgs&, const ChemParams&, cudaStream_t);  \
-  extern template cudaError_t run_chem2_chain<A, B, true, 4, 2>(const ChainArgs&, const ChemParams&, cudaStream_t);  \
-  extern template cudaError_t run_chem2_chain<A, B, false, 6, 1>(const ChainArgs&, const ChemParams&, cudaStream_t); \
-  extern template cudaError_t run_chem2_chain<A, B, false, 6, 2>(const ChainArgs&, const ChemParams&, cudaStream_t); \
-  extern template cudaError_t run_chem2_chain<A, B, false, 3, 1>(const ChainArgs&, const ChemParams&, cudaStream_t); \
-  extern template cudaError_t run_chem2_chain<A, B, false, 3, 2>(const ChainArgs&, const ChemParams&, cudaStream_t); \
-  extern template cudaError_t run_chem2_rhs<A, B>(const double*, double*, size_t, int, const ChemParams&, cudaStream_t);
-MR_DECL2(18, 3)
-#undef MR_DECL2
 }  // namespace mrchem
 
 // (NW warps = slots, SPL components per thread) layouts: C1/C2 (10
@@ -46,12 +35,8 @@ int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int nd
   cfg->subdiag = subdiag;
   cfg->nstage = tab.s;
   cfg->ndeg = ndeg;
-  cfg->cpt = 1;
   if (ncomp <= 12) { cfg->NW = 4; cfg->SPL = 3; }
   else if (ncomp <= 24) { cfg->NW = 8; cfg->SPL = 3; }
-#ifndef MR_CHEM_ONE_CELL  // A/B builds only: the one-cell-per-thread kernel for every size
-  else if (ncomp <= 54 && 4 * 18 <= 2 * ncomp) { cfg->NW = 18; cfg->SPL = 3; cfg->cpt = 2; }
-#endif
   else if (ncomp <= 64) { cfg->NW = 32; cfg->SPL = 2; }
   else return 1;
   return 0;
@@ -65,9 +50,8 @@ int chem_chunking(const ChemCfg& cfg, int S, int R, size_t blob_bytes, int* rc, 
   const int NW = cfg.NW;
   const size_t budget = (size_t)(NW <= 8 ? 113 : 227) * 1024;
   const int words = (int)((blob_bytes + 15) / 16);
-  const size_t fixed = cfg.cpt == 2 ? mrchem::smem2_bytes(NW, S + 1, 0, words)
-                                    : mrchem::smem_bytes(NW, S + 1, 0, words);
-  const size_t row = cfg.cpt == 2 ? mrchem::kC2Row : 256;
+  const size_t fixed = mrchem::smem_bytes(NW, S + 1, 0, words);
+  const size_t row = 256;
   if (fixed >= budget) return 1;
   int cap = (int)((budget - fixed) / row);
   cap -= cap % NW;
@@ -91,20 +75,6 @@ cudaError_t launch_chem_chain(const ChemCfg& cfg, const ChainArgs& a, const Chem
     if (!cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem_chain<A, B, false, 6, 1>(a, P, st); \
     if (!cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem_chain<A, B, false, 6, 2>(a, P, st); \
   }
-  if (cfg.cpt == 2) {
-#define MR_CHEM2_DISPATCH(A, B)                                                                      \
-    if (cfg.NW == A && cfg.SPL == B) {                                                               \
-      if (cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem2_chain<A, B, true, 4, 1>(a, P, st);  \
-      if (cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem2_chain<A, B, true, 4, 2>(a, P, st);  \
-      if (!cfg.subdiag && cfg.nstage <= 3 && cfg.ndeg == 1) return mrchem::run_chem2_chain<A, B, false, 3, 1>(a, P, st); \
-      if (!cfg.subdiag && cfg.nstage <= 3 && cfg.ndeg == 2) return mrchem::run_chem2_chain<A, B, false, 3, 2>(a, P, st); \
-      if (!cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem2_chain<A, B, false, 6, 1>(a, P, st); \
-      if (!cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem2_chain<A, B, false, 6, 2>(a, P, st); \
-    }
-    MR_CHEM2_DISPATCH(18, 3)
-#undef MR_CHEM2_DISPATCH
-    return cudaErrorInvalidConfiguration;
-  }
   if (cfg.NW == 32 && cfg.SPL == 2 && !cfg.subdiag && cfg.nstage <= 3) {
     if (cfg.ndeg == 1) return mrchem::run_chem_chain<32, 2, false, 3, 1>(a, P, st);
     if (cfg.ndeg == 2) return mrchem::run_chem_chain<32, 2, false, 3, 2>(a, P, st);
@@ -117,10 +87,6 @@ cudaError_t launch_chem_chain(const ChemCfg& cfg, const ChainArgs& a, const Chem
 cudaError_t launch_chem_rhs(const ChemCfg& cfg, const double* y, double* out, size_t ncell,
                             int ncomp, const ChemParams& P, cudaStream_t st)
 {
-  if (cfg.cpt == 2) {
-    if (cfg.NW == 18 && cfg.SPL == 3) return mrchem::run_chem2_rhs<18, 3>(y, out, ncell, ncomp, P, st);
-    return cudaErrorInvalidConfiguration;
-  }
 #define MR_CHEM_RHS(A, B) \
   if (cfg.NW == A && cfg.SPL == B) return mrchem::run_chem_rhs<A, B>(y, out, ncell, ncomp, P, st);
   MR_CHEM_BLOCK_LAYOUTS(MR_CHEM_RHS)

@@ -1441,11 +1441,11 @@ static int domain_rhs(mr_ctx* d, int kind, const double* y, double* out)
 
 #define MR_FORWARD(c, expr)                                            \
   do {                                                                 \
-    if (!(c)->slabs.empty()) return for_slabs((c), [&](mr_ctx* sl_) { return (expr); }); \
+    if ((c) && !(c)->slabs.empty()) return for_slabs((c), [&](mr_ctx* sl_) { return (expr); }); \
   } while (0)
 #define MR_NOT_ON_DOMAIN(c, what)                                                          \
   do {                                                                                     \
-    if (!(c)->slabs.empty())                                                               \
+    if ((c) && !(c)->slabs.empty())                                                        \
       return set_err((c), MR_CONTRACT, std::string(what) + ": not available on a multi-device domain"); \
   } while (0)
 
@@ -1780,19 +1780,15 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
         load[best] += cost[k];
       }
     }
-    // shared-memory row sizes of the layout: one cell per thread (32-cell
-    // rows: (C, E') double2 rows of 512 B, D' and q rows of 256 B) or two
-    // cells per thread (64-cell rows of 512 B; C, E', D' separate tables at
-    // fixed distances, so every species offset is k * 512)
-    const unsigned prow = lay.cpt == 2 ? 512u : 256u, qrow = prow;
     std::vector<ChemRec> recs(R);
     for (int j = 0; j < R; ++j) {
       ChemRec& r = recs[j];
       std::memset(&r, 0, sizeof(r));
       r.lnA = rx[j].x; r.beta = rx[j].y; r.EaR = rx[j].z;
       r.r1o = (unsigned)rs[j].x * 512u; r.r2o = (unsigned)rs[j].y * 512u;
-      r.p1o = (unsigned)rs[j].z * prow; r.p2o = (unsigned)rs[j].w * prow;
+      r.p1o = (unsigned)rs[j].z * 256u; r.p2o = (unsigned)rs[j].w * 256u;
     }
+    const unsigned qrow = 256u;
     const unsigned zero_off = (unsigned)rcz * qrow;  // all-zero row right after q
     std::vector<unsigned> ents;
     for (int k = 0; k < S; ++k)

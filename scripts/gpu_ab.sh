@@ -1,12 +1,13 @@
-# A/B timing of env settings on C4 physics at 64^3: each arg = "NAME=VAL" or "-"
+# A/B of library variants (MR_LIB_PATH) on one workload: ms per step and the
+# chemistry share.  Usage: bash scripts/gpu_ab.sh "C4 128" lib1 lib2 ... ("-" = in-tree)
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-i=0
-for E in "$@"; do
-  i=$((i+1))
-  if [ "$E" = "-" ]; then EV=""; else EV="$E"; fi
-  env $EV timeout 300 python bench.py --n 64 --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_out/ab_$i.log 2>&1
-  python -c "
-import json; d=json.loads(open('gpurun_out/ab_$i.log').read().strip().split('\n')[-1])
-print('$E', 'ms/step %.2f'%d['ms_per_step'], 'chem TF %.2f frac %.3f'%(d['roofline']['achieved'], d['roofline']['frac']))" || tail -3 gpurun_out/ab_$i.log
+read CFG N <<< "$1"; shift
+for L in "$@"; do
+  if [ "$L" = "-" ]; then unset MR_LIB_PATH; else export MR_LIB_PATH=$PWD/$L; fi
+  timeout 600 python bench.py --config $CFG --n $N --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_out/ab.log 2>&1
+  echo "$CFG n=$N lib=$L: $(tail -1 gpurun_out/ab.log | python -c 'import json,sys
+try:
+  d=json.loads(sys.stdin.read()); print("ms/step %.1f chem ms/step %.1f frac %.3f" % (d["ms_per_step"], d["time_split_ms"]["chem"]/d["steps"], d["roofline"]["frac"]))
+except Exception as e: print("FAILED", e)')"
 done
