@@ -13,6 +13,7 @@
 // Counters follow the reference's increment rules exactly (mri.cpp:342, :347,
 // :378; erk.cpp:28), including partial counts on an IntegrationError.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a tool attaches
 #include "nccl_shim.h"
 
 #include <algorithm>
@@ -249,6 +250,24 @@ int set_err(mr_ctx* c, int code, const std::string& msg)
   if (c) c->err = msg;
   return code;
 }
+
+// NVTX range for the host-side stage loop (nsys / ncu --nvtx show the MRI
+// stage structure of a step; free when no tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* kind, int a, int b = -1)
+  {
+    char buf[64];
+    if (b >= 0)
+      std::snprintf(buf, sizeof(buf), "%s %d..%d", kind, a, b);
+    else
+      std::snprintf(buf, sizeof(buf), "%s %d", kind, a);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // stream / device of slab c inside a step whose shared stream is st: the slabs
 // of a multi-device domain each run on their own stream and device, the
@@ -1091,12 +1110,23 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
   int missing_stage = -1;
   unsigned long long host_key = MR_NO_FAIL;  // Newton failure (host decision)
 
+  NvtxRange step_range("mri_step");
   for (const Op& o : plan.ops) {
     if (o.type == Op::COUNT_SLOW) continue;
     if (o.type == Op::MISSING) {
       missing_stage = o.stage;
       break;
     }
+    // one NVTX range per stage-plan op: slow evaluation f_E(j), implicit
+    // evaluation f_I(j), implicit solve of stage i, explicit update of stage
+    // i, fused chain of cell-local stages i..k
+    const NvtxRange op_range(o.type == Op::SLOW     ? "slow f_E"
+                             : o.type == Op::IMPL   ? "implicit f_I"
+                             : o.type == Op::SOLVE  ? "implicit solve"
+                             : o.type == Op::UPDATE ? "explicit update"
+                                                    : "fast IVP chain",
+                             o.type == Op::CHAIN ? o.stages.front() : o.stage,
+                             o.type == Op::CHAIN ? o.stages.back() : -1);
     // profile classes: 0 fused fast IVPs, 1 explicit slow RHS (stencil),
     // 2 everything else (updates, implicit evaluations and solves)
     const int cls = o.type == Op::CHAIN ? 0 : (o.type == Op::SLOW ? 1 : 2);
@@ -2213,6 +2243,7 @@ int ark_explicit(mr_ctx** cs, int n, double* const* in, double* const* out, cuda
 
 int ark_domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int* fail_stage)
 {
+  const NvtxRange range("ark_imex_step");
   mr_ctx* c0 = cs[0];
   if (fail_stage) *fail_stage = -1;
   if (!(H > 0.0)) return set_err(c0, MR_CONTRACT, "ark_imex_step: H must be positive");
