@@ -1840,6 +1840,22 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
         P.lst[k][ch2] = make_ushort4(st4[0], n4[0], st4[1], n4[1]);
       }
     while (ents.size() % 4) ents.push_back(zero_off);
+    // every shared-memory offset the kernel will add to a lane address stays
+    // inside its table (compute-sanitizer is not available on the GPU pool:
+    // the bounds of all data-dependent shared accesses are checked here)
+    for (const ChemRec& r : recs)
+      if (r.r1o >= (unsigned)(S + 1) * 512u || r.r2o >= (unsigned)(S + 1) * 512u ||
+          r.p1o >= (unsigned)(S + 1) * 256u || r.p2o >= (unsigned)(S + 1) * 256u)
+        return set_err(c, MR_CONTRACT, "mr_fast_chemistry: species offset outside its table");
+    for (unsigned e : ents)
+      if (e > zero_off || e % 256u)
+        return set_err(c, MR_CONTRACT, "mr_fast_chemistry: production entry outside the rate buffer");
+    for (int k = 0; k < S; ++k)
+      for (int ch2 = 0; ch2 < nch; ++ch2) {
+        const ushort4 L = P.lst[k][ch2];
+        if ((size_t)(L.x + L.y) * 4 > ents.size() || (size_t)(L.z + L.w) * 4 > ents.size())
+          return set_err(c, MR_CONTRACT, "mr_fast_chemistry: production list outside the blob");
+      }
     const size_t rec_bytes = (size_t)R * sizeof(ChemRec);
     const size_t blob_bytes = rec_bytes + ents.size() * 4;
     if (blob_bytes > blob_bound)
