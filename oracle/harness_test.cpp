@@ -195,3 +195,32 @@ extern "C" int harness_selftest(int n, int S, int R, double rho, const double* s
     return 1;
   }
 }
+
+// The routed harness on a CPU problem: the reference's own convergence study
+// (execute_study, harness.cpp:431-512) of its LinearTwoRateOde through the
+// routing functions, which must fall through to the reference's integrators.
+// slopes[i] = fitted slope of methods[i] (comma list); returns the row count.
+extern "C" int harness_cpu_study(const char* methods, const double* hs, int nh, const char* csv,
+                                 double* slopes, char* err, size_t errlen)
+{
+  try {
+    StudyConfig cfg;
+    cfg.problem_kind = "linear-two-rate";
+    cfg.methods = split(methods);
+    cfg.h_list.assign(hs, hs + nh);
+    cfg.t0 = 0.0;
+    cfg.tf = 1.0;
+    cfg.reference_method = "analytic";
+    cfg.jobs = 1;
+    const RunReport rep = run_convergence_study(cfg);
+    rep.write_csv(csv);
+    for (std::size_t i = 0; i < cfg.methods.size(); ++i) {
+      const auto it = rep.fitted_slopes.find(cfg.methods[i]);
+      slopes[i] = it == rep.fitted_slopes.end() ? std::nan("") : it->second;
+    }
+    return (int)rep.rows.size();
+  } catch (const std::exception& e) {
+    if (err && errlen) std::snprintf(err, errlen, "%s", e.what());
+    return -1;
+  }
+}

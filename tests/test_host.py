@@ -167,3 +167,28 @@ def test_reference_harness_is_routed_unmodified():
     defs = subprocess.run(["nm", "-C", "--defined-only", lib], capture_output=True, text=True).stdout
     for f in ("mri_integrate_routed", "run_method", "harness_selftest", "RunReport::write_csv"):
         assert f in defs, f
+
+
+def test_routed_harness_runs_cpu_studies_unchanged(tmp_path):
+    """The reference's convergence study (execute_study, harness.cpp:431-512)
+    through the routed harness build on its own LinearTwoRateOde: no device
+    problem is routed, so every run falls through to the reference's
+    integrators and the methods converge at their orders."""
+    lib = os.path.join(ROOT, "oracle", "_ref", "libharness_test.so")
+    if not os.path.exists(lib):
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    L = C.CDLL(lib)
+    dp = C.POINTER(C.c_double)
+    L.harness_cpu_study.argtypes = [C.c_char_p, dp, C.c_int, C.c_char_p, dp, C.c_char_p, C.c_size_t]
+    methods = ["mri3-10", "erk-classic-rk4", "imex-mri3-10", "ark-imex"]
+    hs = np.array([0.1, 0.05, 0.025, 0.0125])
+    slopes = np.zeros(len(methods))
+    err = C.create_string_buffer(256)
+    csv_path = str(tmp_path / "study.csv")
+    n = L.harness_cpu_study(",".join(methods).encode(), hs.ctypes.data_as(dp), len(hs),
+                            csv_path.encode(), slopes.ctypes.data_as(dp), err, 256)
+    assert n == len(methods) * len(hs), err.value.decode()
+    rows = open(csv_path).read().strip().splitlines()
+    assert rows[0].startswith("method,H,tolerance,error,rate") and len(rows) == n + 1
+    for name, order, s in zip(methods, [3, 4, 3, 4], slopes):
+        assert s > order - 0.5, (name, s)
