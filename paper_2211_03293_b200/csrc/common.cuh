@@ -50,7 +50,6 @@ struct ChainArgs {
   size_t ncell;
   int ncomp;
   unsigned long long* fail;
-  double* rcs;  // forcing-coefficient scratch [ndeg][ncomp][ncell] (warp-specialised chemistry kernel)
 };
 
 // Mechanism for the chemistry kernel.  Scalars and per-species data travel
@@ -88,8 +87,7 @@ struct ChemParams {
 };
 
 struct ChemCfg {
-  int NW, SPL;  // warps per cell group (slots), components per thread
-  int NG;       // cell groups per block (2: warp-specialised kernel, kernels_chem_ws.cuh)
+  int NW, SPL;  // warps per block (slots), components per thread
   bool subdiag;
   int nstage;  // inner table stages (non-subdiagonal tables: stage accumulators)
   int ndeg;

@@ -3,7 +3,7 @@
 // (kernels_chem_nw*.cu).  Kernel design: kernels_chem.cuh.
 #include <cuda_runtime.h>
 
-#include "kernels_chem_ws.cuh"
+#include "kernels_chem.cuh"
 
 namespace mrchem {
 #define MR_DECL(A, B)                                                                      \
@@ -18,31 +18,7 @@ MR_DECL(32, 2)
 #undef MR_DECL
 extern template cudaError_t run_chem_chain<32, 2, false, 3, 1>(const ChainArgs&, const ChemParams&, cudaStream_t);
 extern template cudaError_t run_chem_chain<32, 2, false, 3, 2>(const ChainArgs&, const ChemParams&, cudaStream_t);
-#define MR_DECL_WS(SUB, MS, ND) \
-  extern template cudaError_t run_chem_chain_ws<2, SUB, MS, ND>(const ChainArgs&, const ChemParams&, cudaStream_t);
-MR_DECL_WS(true, 4, 1)
-MR_DECL_WS(true, 4, 2)
-MR_DECL_WS(false, 6, 1)
-MR_DECL_WS(false, 6, 2)
-MR_DECL_WS(false, 3, 1)
-MR_DECL_WS(false, 3, 2)
-#undef MR_DECL_WS
 }  // namespace mrchem
-
-// Warp-specialised chain (kernels_chem_ws.cuh) for the 25-64-component
-// mechanisms whose whole rate buffer fits next to two groups' species rows;
-// MR_CHEM_WS=0 builds the single-group kernel everywhere (A/B measurements).
-#ifndef MR_CHEM_WS
-#define MR_CHEM_WS 1
-#endif
-static int ws_rc(int R) { return (R + mrchem::kWsWorkers - 1) / mrchem::kWsWorkers * mrchem::kWsWorkers; }
-static bool ws_fits(int S, int R)
-{
-  if (!MR_CHEM_WS) return false;
-  // blob bound: records + entries (<= 4 per reaction) + per-list padding
-  const size_t blob = (size_t)R * sizeof(ChemRec) + 4 * (4 * (size_t)R + 2 * 3 * (size_t)S) + 16;
-  return mrchem::ws_smem_bytes(S + 1, ws_rc(R), (int)((blob + 15) / 16)) <= (size_t)227 * 1024;
-}
 
 // (NW warps = slots, SPL components per thread) layouts: C1/C2 (10
 // components), C3 (22), C4/C5 (54); DESIGN.md section 4 for the measurements
@@ -50,6 +26,7 @@ static bool ws_fits(int S, int R)
 
 int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int ndeg)
 {
+  (void)R;
   if (S + 1 > MR_CHEM_MAXS || ndeg < 1 || ndeg > MR_MAXDEG || tab.s > MR_MAXS) return 1;
   bool subdiag = true;
   for (int i = 0; i < tab.s; ++i)
@@ -62,8 +39,6 @@ int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int nd
   else if (ncomp <= 24) { cfg->NW = 8; cfg->SPL = 3; }
   else if (ncomp <= 64) { cfg->NW = 32; cfg->SPL = 2; }
   else return 1;
-  cfg->NG = 1;
-  if (ncomp > 24 && ws_fits(S, R)) { cfg->NW = mrchem::kWsWorkers; cfg->SPL = 2; cfg->NG = 2; }
   return 0;
 }
 
@@ -73,14 +48,6 @@ int chem_pick(ChemCfg* cfg, int ncomp, int S, int R, const TableDev& tab, int nd
 int chem_chunking(const ChemCfg& cfg, int S, int R, size_t blob_bytes, int* rc, int* nchunk)
 {
   const int NW = cfg.NW;
-  if (cfg.NG == 2) {  // one chunk holding every reaction, the two groups take turns
-    const int size = ws_rc(R);
-    const int words = (int)((blob_bytes + 15) / 16);
-    if (mrchem::ws_smem_bytes(S + 1, size, words) > (size_t)227 * 1024) return 1;
-    *rc = size;
-    *nchunk = 1;
-    return 0;
-  }
   const size_t budget = (size_t)(NW <= 8 ? 113 : 227) * 1024;
   const int words = (int)((blob_bytes + 15) / 16);
   const size_t fixed = mrchem::smem_bytes(NW, S + 1, 0, words);
@@ -108,18 +75,6 @@ cudaError_t launch_chem_chain(const ChemCfg& cfg, const ChainArgs& a, const Chem
     if (!cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem_chain<A, B, false, 6, 1>(a, P, st); \
     if (!cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem_chain<A, B, false, 6, 2>(a, P, st); \
   }
-  if (cfg.NG == 2) {
-    if (a.rcs == nullptr) return cudaErrorInvalidValue;
-    if (cfg.subdiag && cfg.ndeg == 1) return mrchem::run_chem_chain_ws<2, true, 4, 1>(a, P, st);
-    if (cfg.subdiag && cfg.ndeg == 2) return mrchem::run_chem_chain_ws<2, true, 4, 2>(a, P, st);
-    if (cfg.nstage <= 3) {
-      if (cfg.ndeg == 1) return mrchem::run_chem_chain_ws<2, false, 3, 1>(a, P, st);
-      if (cfg.ndeg == 2) return mrchem::run_chem_chain_ws<2, false, 3, 2>(a, P, st);
-    }
-    if (cfg.ndeg == 1) return mrchem::run_chem_chain_ws<2, false, 6, 1>(a, P, st);
-    if (cfg.ndeg == 2) return mrchem::run_chem_chain_ws<2, false, 6, 2>(a, P, st);
-    return cudaErrorInvalidConfiguration;
-  }
   if (cfg.NW == 32 && cfg.SPL == 2 && !cfg.subdiag && cfg.nstage <= 3) {
     if (cfg.ndeg == 1) return mrchem::run_chem_chain<32, 2, false, 3, 1>(a, P, st);
     if (cfg.ndeg == 2) return mrchem::run_chem_chain<32, 2, false, 3, 2>(a, P, st);
@@ -132,10 +87,6 @@ cudaError_t launch_chem_chain(const ChemCfg& cfg, const ChainArgs& a, const Chem
 cudaError_t launch_chem_rhs(const ChemCfg& cfg, const double* y, double* out, size_t ncell,
                             int ncomp, const ChemParams& P, cudaStream_t st)
 {
-  // a single evaluation of the warp-specialised layout runs on the
-  // single-group kernel (any slot -> component permutation of its 64 slots
-  // is valid for it; the rate buffer is one chunk)
-  if (cfg.NG == 2) return mrchem::run_chem_rhs<32, 2>(y, out, ncell, ncomp, P, st);
 #define MR_CHEM_RHS(A, B) \
   if (cfg.NW == A && cfg.SPL == B) return mrchem::run_chem_rhs<A, B>(y, out, ncell, ncomp, P, st);
   MR_CHEM_BLOCK_LAYOUTS(MR_CHEM_RHS)

@@ -204,8 +204,6 @@ struct mr_ctx {
   size_t halo_elems = 0;
   double *scr_in = nullptr, *scr_out = nullptr;
   double* y_backup = nullptr;  // state at the start of an integrate call (restored on failure)
-  double* rcs = nullptr;       // forcing-coefficient scratch of the warp-specialised chemistry kernel
-  size_t rcs_elems = 0;
   unsigned long long* d_fail = nullptr;
   unsigned long long* h_fail = nullptr;
   double* d_red = nullptr;  // partials + out
@@ -322,8 +320,6 @@ void free_state(mr_ctx* c)
   free_dev_t(c->scr_in);
   free_dev_t(c->scr_out);
   free_dev_t(c->y_backup);
-  free_dev_t(c->rcs);
-  c->rcs_elems = 0;
   free_dev_t(c->cg_known);
   free_dev_t(c->cg_r);
   free_dev_t(c->cg_z);
@@ -1183,16 +1179,6 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
         a.ncomp = c->ncomp;
         a.fail = c->d_fail;
         sdev(c);
-        if (c->fast_kind == FK_CHEM && ccfg.NG == 2) {
-          const size_t need = (size_t)a.ndeg * c->dof;
-          if (c->rcs_elems < need) {
-            free_dev_t(c->rcs);
-            c->rcs_elems = 0;
-            MR_CUDA_TRY(c, cudaMalloc(&c->rcs, need * sizeof(double)));
-            c->rcs_elems = need;
-          }
-          a.rcs = c->rcs;
-        }
         if (c->fast_kind == FK_CHEM)
           MR_CUDA_TRY(c, launch_chem_chain(ccfg, a, *c->chemP, sst(c, st)));
         else
