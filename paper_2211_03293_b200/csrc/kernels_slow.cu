@@ -875,6 +875,29 @@ __device__ __forceinline__ double red_op(int kind, double a, double b)
   return a + b;
 }
 
+// Block reduction: a butterfly of warp shuffles inside each warp, the warp
+// results through shared memory, a second butterfly in warp 0.  The pairing
+// is fixed by lane and warp index, so the result is run-to-run bitwise.
+// Valid in thread 0; all threads of the block must call it.
+template <int NT>
+__device__ __forceinline__ double block_reduce(int op, double v)
+{
+  static_assert(NT % 32 == 0 && NT <= 1024, "block size");
+  __shared__ double wsum[NT / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = red_op(op, v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();  // wsum may still be read by a previous reduction
+  if (lane == 0) wsum[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    v = lane < NT / 32 ? wsum[lane] : 0.0;  // identity of + and of max over |x|
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = red_op(op, v, __shfl_xor_sync(0xffffffffu, v, o));
+  }
+  return v;
+}
+
 template <int KIND>
 __device__ __forceinline__ double red_term(const double* __restrict__ x,
                                            const double* __restrict__ w, size_t i)
@@ -906,31 +929,19 @@ __global__ void __launch_bounds__(kRedThreads) reduce_partial(const double* __re
   }
   for (; i < n; i += stride) a0 = red_op(OP, a0, red_term<KIND>(x, w, i));
   const double acc = red_op(OP, red_op(OP, a0, a1), red_op(OP, a2, a3));
-  __shared__ double sh[kRedThreads];
-  sh[threadIdx.x] = acc;
-  __syncthreads();
-  for (int o = kRedThreads / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sh[threadIdx.x] = red_op(OP, sh[threadIdx.x], sh[threadIdx.x + o]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+  const double r = block_reduce<kRedThreads>(OP, acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = r;
 }
 
 __global__ void __launch_bounds__(1024) reduce_final(int kind, const double* __restrict__ part,
                                                     int np, size_t n, double* __restrict__ out)
 {
-  __shared__ double sh[1024];
   const int op = kind == RED_NONFINITE ? RED_TWO : kind;
   double acc = 0.0;
   for (int i = threadIdx.x; i < np; i += blockDim.x) acc = red_op(op, acc, part[i]);
-  sh[threadIdx.x] = acc;
-  __syncthreads();
-  for (int o = 512; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sh[threadIdx.x] = red_op(op, sh[threadIdx.x], sh[threadIdx.x + o]);
-    __syncthreads();
-  }
+  acc = block_reduce<1024>(op, acc);
   if (threadIdx.x == 0) {
-    double r = sh[0];
+    double r = acc;
     if (kind == RED_WRMS) r = sqrt(r / (double)n);
     else if (kind == RED_TWO) r = sqrt(r);
     out[0] = r;
@@ -1132,15 +1143,8 @@ __device__ __forceinline__ double lap7_row(const LapArgs& a, const double* __res
 
 __device__ __forceinline__ void block_sum_store(double v, double* part)
 {
-  __shared__ double sh[kLapThreads];
-  __syncthreads();  // sh may still be read by a previous reduction
-  sh[threadIdx.x] = v;
-  __syncthreads();
-  for (int o = kLapThreads / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+  v = block_reduce<kLapThreads>(RED_DOT, v);
+  if (threadIdx.x == 0) part[blockIdx.x] = v;
 }
 
 // MODE 0: o1 = D L7 y                                     (f_implicit evaluation)
@@ -1393,16 +1397,10 @@ __global__ void __launch_bounds__(kLapThreads) cg_p_kernel(size_t n, const doubl
 __global__ void __launch_bounds__(1024) part_sum_kernel(const double* part, int np, double* sc,
                                                         int slot)
 {
-  __shared__ double sh[1024];
   double acc = 0.0;
   for (int i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
-  sh[threadIdx.x] = acc;
-  __syncthreads();
-  for (int o = 512; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) sc[slot] = sh[0];
+  acc = block_reduce<1024>(RED_DOT, acc);
+  if (threadIdx.x == 0) sc[slot] = acc;
 }
 
 // global value = sum of the slabs' values in slab order, written to every slab
