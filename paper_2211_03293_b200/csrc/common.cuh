@@ -47,9 +47,12 @@ struct ChainArgs {
   const double* y_in;
   double* y_out;
   const double* fE[MR_MAXSLOT];
-  size_t ncell;
+  size_t ncell;  // cells of the slab (the stride of a component)
   int ncomp;
   unsigned long long* fail;
+  size_t cell0, cell1;  // cells [cell0, cell1) this launch advances (chemistry
+                        // chain; cell1 == 0: all), e.g. the plane chunks of a
+                        // host-buffer step whose upload is still in flight
 };
 
 // Mechanism for the chemistry kernel.  Scalars and per-species data travel

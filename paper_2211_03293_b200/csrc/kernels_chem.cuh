@@ -351,8 +351,8 @@ __global__ void __launch_bounds__(NW * 32, chem_min_blocks(NW, NDEG))
   extern __shared__ __align__(16) double smem_raw[];
   const int c = threadIdx.x & 31;
   const int w = (int)(threadIdx.x >> 5);
-  const size_t cell = (size_t)blockIdx.x * 32 + c;
-  const bool active = cell < a.ncell;
+  const size_t cell = a.cell0 + (size_t)blockIdx.x * 32 + c;
+  const bool active = cell < (a.cell1 ? a.cell1 : a.ncell);
   const size_t nc = a.ncell;
   const int ncomp = a.ncomp;
 #ifdef MR_PHASE_PROF
@@ -554,7 +554,9 @@ cudaError_t run_chem_chain(const ChainArgs& a, const ChemParams& P, cudaStream_t
   auto k = chem_chain_kernel<NW, SPL, SUBDIAG, MAXS, NDEG>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const size_t blocks = (a.ncell + 31) / 32;
+  const size_t cells = (a.cell1 ? a.cell1 : a.ncell) - a.cell0;
+  if (cells == 0) return cudaSuccess;
+  const size_t blocks = (cells + 31) / 32;
   k<<<(unsigned)blocks, NW * 32, smem, st>>>(a, P);
   return cudaGetLastError();
 }

@@ -151,6 +151,8 @@ struct Plan {
 
 }  // namespace
 
+constexpr int kHeadChunks = 16;  // plane chunks of a pipelined host-buffer upload
+
 struct mr_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -212,6 +214,11 @@ struct mr_ctx {
   // comm
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
+  // mr_mri_step_host: the upload of the caller's state rides on the step's
+  // first stencil + fused chain, plane chunk by plane chunk (domain_step)
+  const double* host_in = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copy[kHeadChunks + 1] = {};
   cudaStream_t comm_stream = nullptr;  // halo exchange overlapped with the interior stencil
   cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
   // instrumentation
@@ -1050,6 +1057,88 @@ int domain_finish(mr_ctx** cs, int n, const Plan& plan, double t, double H, int 
 
 // async: enqueue only (n == 1); the step is finished by domain_finish from
 // mr_mri_step_wait with the state kept in ctx->pending
+// Host-buffer step, upload overlapped with compute: the state arrives in
+// plane chunks on a copy stream (last chunk first, it is the periodic ghost of
+// the first); the step's first two ops -- the stage-0 slow evaluation and the
+// fused chain of the first cell-local stages -- run chunk by chunk on the
+// compute stream as soon as a chunk and its neighbour have landed.  Same
+// kernels and arithmetic as the whole-grid ops (bitwise equal), the PCIe copy
+// hides behind the chemistry.  Returns the number of plan ops it executed
+// (0: not applicable -- the caller uploads in one copy).
+int head_upload(mr_ctx* c, const double* hin, const Plan& plan, double t, double H,
+                const ChemCfg& ccfg, cudaStream_t st, int* nops)
+{
+  *nops = 0;
+  const int M = c->M;
+  const int K = std::min(kHeadChunks, M > 0 ? c->n0l / M : 0);
+  if (c->comm || c->in_domain || c->profile || c->fast_kind != FK_CHEM ||
+      c->slow_kind != SK_STENCIL || c->imex || K < 3 || plan.ops.size() < 2 ||
+      plan.ops[0].type != Op::SLOW || plan.ops[0].stage != 0 || plan.ops[1].type != Op::CHAIN)
+    return MR_OK;
+  StencilArgs sa = stencil_args(c, c->y_state, c->slots[plan.slot_of[0]], nullptr, nullptr);
+  if (!stencil_plane_ranges(sa)) return MR_OK;
+  int rc = ensure_halo(c);
+  if (rc) return rc;
+  if (!c->copy_stream) {
+    MR_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : c->ev_copy)
+      MR_CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  int pb[kHeadChunks + 1];
+  for (int q = 0; q <= K; ++q) pb[q] = (int)((long long)q * c->n0l / K);
+  // the copies start after whatever the compute stream still does with y_state
+  MR_CUDA_TRY(c, cudaEventRecord(c->ev_copy[kHeadChunks], st));
+  MR_CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->ev_copy[kHeadChunks], 0));
+  const size_t pitch = c->ncell * sizeof(double);
+  for (int i = 0; i < K; ++i) {
+    const int q = (i + K - 1) % K;  // K-1, 0, 1, ..., K-2
+    const size_t off = (size_t)pb[q] * c->plane;
+    MR_CUDA_TRY(c, cudaMemcpy2DAsync(c->y_state + off, pitch, hin + off, pitch,
+                                     (size_t)(pb[q + 1] - pb[q]) * c->plane * sizeof(double),
+                                     c->ncomp, cudaMemcpyHostToDevice, c->copy_stream));
+    MR_CUDA_TRY(c, cudaEventRecord(c->ev_copy[q], c->copy_stream));
+  }
+  // periodic ghosts: the first and the last M planes (chunks 0 and K-1)
+  MR_CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_copy[0], 0));
+  MR_CUDA_TRY(c, launch_halo_pack(c->y_state, c->send_lo, c->send_hi, c->ncomp, c->n0l, c->plane,
+                                  M, st));
+  c->launches++;
+  sa.halo_lo = c->send_hi;
+  sa.halo_hi = c->send_lo;
+  const Op& o = plan.ops[1];
+  ChainArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.nst = (int)o.stages.size();
+  a.ndeg = ndeg_of(c);
+  for (int q = 0; q < a.nst; ++q) fill_chain_stage(c, o.stages[q], t, H, plan, a.st[q]);
+  a.tab = c->tab;
+  a.y_in = c->y_state;
+  a.y_out = c->y_work;
+  for (int q = 0; q < (int)c->slots.size() && q < MR_MAXSLOT; ++q) a.fE[q] = c->slots[q];
+  a.ncell = c->ncell;
+  a.ncomp = c->ncomp;
+  a.fail = c->d_fail;
+  {
+    const NvtxRange r0("slow f_E", 0, -1);
+    const NvtxRange r1("fast IVP chain", o.stages.front(), o.stages.back());
+    for (int q = 0; q < K; ++q) {
+      // chunks q - 1, q and q + 1 (the ghosts of chunks 0 and K-1 are packed);
+      // the copy stream is in order K-1, 0, 1, ..., K-2, so one event covers
+      // all three: chunk q + 1's, or chunk K-2's for the last two chunks
+      MR_CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_copy[q + 1 <= K - 2 ? q + 1 : K - 2], 0));
+      sa.i_lo = pb[q];
+      sa.i_hi = pb[q + 1];
+      MR_CUDA_TRY(c, launch_stencil(sa, st));
+      a.cell0 = (size_t)pb[q] * c->plane;
+      a.cell1 = (size_t)pb[q + 1] * c->plane;
+      MR_CUDA_TRY(c, launch_chem_chain(ccfg, a, *c->chemP, st));
+      c->launches += 2;
+    }
+  }
+  *nops = 2;
+  return MR_OK;
+}
+
 int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int* fail_stage,
                 bool async = false)
 {
@@ -1111,7 +1200,25 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
   unsigned long long host_key = MR_NO_FAIL;  // Newton failure (host decision)
 
   NvtxRange step_range("mri_step");
-  for (const Op& o : plan.ops) {
+  size_t first_op = 0;
+  if (n == 1 && c0->host_in) {  // host-buffer step: upload (pipelined when possible)
+    const double* hin = c0->host_in;
+    c0->host_in = nullptr;
+    int nops = 0;
+    if (!async && c0->fast_kind == FK_CHEM) {
+      int rc = head_upload(c0, hin, plan, t, H, ccfg, st, &nops);
+      if (rc) return rc;
+    }
+    if (nops == 0) {
+      MR_CUDA_TRY(c0, cudaMemcpyAsync(c0->y_state, hin, c0->dof * sizeof(double),
+                                      cudaMemcpyHostToDevice, st));
+    } else {
+      ycur[0] = c0->y_work;
+      first_op = (size_t)nops;
+    }
+  }
+  for (size_t oi = first_op; oi < plan.ops.size(); ++oi) {
+    const Op& o = plan.ops[oi];
     if (o.type == Op::COUNT_SLOW) continue;
     if (o.type == Op::MISSING) {
       missing_stage = o.stage;
@@ -1581,6 +1688,9 @@ void mr_ctx_destroy(mr_ctx* c)
   if (c->ev_async_in) cudaEventDestroy(c->ev_async_in);
   if (c->ev_async_out) cudaEventDestroy(c->ev_async_out);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (cudaEvent_t e : c->ev_copy)
+    if (e) cudaEventDestroy(e);
   if (c->ev_pack) cudaEventDestroy(c->ev_pack);
   if (c->ev_halo) cudaEventDestroy(c->ev_halo);
   if (c->ev_send) cudaEventDestroy(c->ev_send);
@@ -2463,9 +2573,9 @@ int mr_mri_step_host(mr_ctx* c, double t, double H, const double* y_in, double* 
   cudaSetDevice(c->device);
   int rc = ensure_state(c);
   if (rc) return rc;
-  MR_CUDA_TRY(c, cudaMemcpyAsync(c->y_state, y_in, c->dof * sizeof(double),
-                                 cudaMemcpyHostToDevice, c->stream));
+  c->host_in = y_in;  // uploaded by the step itself (domain_step / head_upload)
   rc = mr_mri_step(c, t, H, counters, fail_stage);
+  c->host_in = nullptr;
   if (rc) return rc;
   MR_CUDA_TRY(c, cudaMemcpyAsync(y_out, c->y_state, c->dof * sizeof(double),
                                  cudaMemcpyDeviceToHost, c->stream));

@@ -448,10 +448,13 @@ def test_virtual_rank_slabs_equal_single_gpu_bitwise(P_, n):
 
 
 # ------------------------------------------------- host-buffer step (e2e ABI)
-@pytest.mark.parametrize("name,n", [("C3", 16), ("C4", 8), ("C1", 12)])
+@pytest.mark.parametrize("name,n", [("C3", 16), ("C4", 8), ("C1", 12), ("C3", 64), ("C4", 64)])
 def test_host_buffer_step_equals_device_step(name, n):
     """mr_mri_step_host (pinned or pageable host buffers, H2D + step + D2H)
-    returns exactly the device-resident step's state and counters."""
+    returns exactly the device-resident step's state and counters -- at 64^3
+    (order 8, plane-range stencil) through the pipelined upload, whose
+    chunked stage-0 stencil and first fused chain must be bitwise the
+    whole-grid ops."""
     import torch
     dev, cfg, y0 = gpu_ctx(name, n)
     c_dev = dev.mri_step(0.0, cfg["H"])
