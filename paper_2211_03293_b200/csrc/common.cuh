@@ -165,6 +165,9 @@ cudaError_t launch_chem_rhs(const ChemCfg& cfg, const double* y, double* out, si
 cudaError_t launch_update(const double* y_in, double* y_out, int nref, const double* const* f,
                           const double* coef, size_t n, int mri_stage,
                           unsigned long long* fail, cudaStream_t st);
+cudaError_t launch_update_rows(const double* y_in, double* y_out, int nref, const double* const* f,
+                               const double* coef, size_t row_len, int rows, size_t row_stride,
+                               int mri_stage, unsigned long long* fail, cudaStream_t st);
 cudaError_t launch_stencil(const StencilArgs& a, cudaStream_t st);
 bool stencil_plane_ranges(const StencilArgs& a);  // launch_stencil accepts [i_lo, i_hi) < all planes
 cudaError_t launch_slow_linear(const double* y, double* out, size_t ncell, const LinDev& lin,

@@ -847,6 +847,23 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdArgs a)
   if (bad) atomicMin(a.fail, mr_fail_key(a.mri_stage, 0, 0));
 }
 
+// the same update on `rows` rows of row_len entries, row stride row_stride
+// (a plane chunk of every component: blockIdx.y = component)
+__global__ void __launch_bounds__(256) update_rows_kernel(const UpdArgs a, size_t row_stride)
+{
+  const size_t ro = (size_t)blockIdx.y * row_stride;
+  bool bad = false;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < a.n;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    double y = a.y_in[ro + idx];
+    for (int r = 0; r < a.nref; ++r)
+      if (a.coef[r] != 0.0) y = dadd(y, dmul(a.coef[r], a.f[r][ro + idx]));
+    a.y_out[ro + idx] = y;
+    bad |= !isfinite(y);
+  }
+  if (bad) atomicMin(a.fail, mr_fail_key(a.mri_stage, 0, 0));
+}
+
 __global__ void __launch_bounds__(256) slow_linear_kernel(const double* __restrict__ y,
                                                           double* __restrict__ out, size_t nc,
                                                           const LinDev L)
@@ -1079,6 +1096,28 @@ cudaError_t launch_update(const double* y_in, double* y_out, int nref, const dou
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks == 0) blocks = 1;
   update_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_rows(const double* y_in, double* y_out, int nref, const double* const* f,
+                               const double* coef, size_t row_len, int rows, size_t row_stride,
+                               int mri_stage, unsigned long long* fail, cudaStream_t st)
+{
+  if (rows <= 0 || row_len == 0) return cudaSuccess;
+  UpdArgs a;
+  a.y_in = y_in;
+  a.y_out = y_out;
+  a.nref = nref;
+  for (int r = 0; r < MR_MAXREF; ++r) {
+    a.f[r] = r < nref ? f[r] : nullptr;
+    a.coef[r] = r < nref ? coef[r] : 0.0;
+  }
+  a.n = row_len;
+  a.mri_stage = mri_stage;
+  a.fail = fail;
+  size_t bx = (row_len + 255) / 256;
+  if (bx > 64) bx = 64;
+  update_rows_kernel<<<dim3((unsigned)bx, (unsigned)rows), 256, 0, st>>>(a, row_stride);
   return cudaGetLastError();
 }
 

@@ -217,6 +217,8 @@ struct mr_ctx {
   // mr_mri_step_host: the upload of the caller's state rides on the step's
   // first stencil + fused chain, plane chunk by plane chunk (domain_step)
   const double* host_in = nullptr;
+  double* host_out = nullptr;  // ... and the result streams out during its last ops
+  bool out_streamed = false;   // y_out was backed up to y_backup and is being written
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[kHeadChunks + 1] = {};
   cudaStream_t comm_stream = nullptr;  // halo exchange overlapped with the interior stencil
@@ -1057,85 +1059,207 @@ int domain_finish(mr_ctx** cs, int n, const Plan& plan, double t, double H, int 
 
 // async: enqueue only (n == 1); the step is finished by domain_finish from
 // mr_mri_step_wait with the state kept in ctx->pending
-// Host-buffer step, upload overlapped with compute: the state arrives in
-// plane chunks on a copy stream (last chunk first, it is the periodic ghost of
-// the first); the step's first two ops -- the stage-0 slow evaluation and the
-// fused chain of the first cell-local stages -- run chunk by chunk on the
-// compute stream as soon as a chunk and its neighbour have landed.  Same
-// kernels and arithmetic as the whole-grid ops (bitwise equal), the PCIe copy
-// hides behind the chemistry.  Returns the number of plan ops it executed
-// (0: not applicable -- the caller uploads in one copy).
-int head_upload(mr_ctx* c, const double* hin, const Plan& plan, double t, double H,
-                const ChemCfg& ccfg, cudaStream_t st, int* nops)
+// ---- pipelined host-buffer step (mr_mri_step_host) ----
+// The state travels in K plane chunks (>= M planes each) on a copy stream
+// while the step computes: the upload rides on the step's first two ops (the
+// stage-0 slow evaluation and the first fused chain), the download on its
+// last three (the last fused chain, the last slow evaluation and the final
+// explicit update).  Those ops run chunk by chunk on the compute stream, in an
+// order that respects the stencil's +-M-plane reach; every kernel computes
+// exactly what the whole-grid op computes (bitwise equal results), only the
+// PCIe copies now hide behind the chemistry.
+int host_chunks(const mr_ctx* c, int* pb)
 {
-  *nops = 0;
-  const int M = c->M;
-  const int K = std::min(kHeadChunks, M > 0 ? c->n0l / M : 0);
+  const int K = std::min(kHeadChunks, c->M > 0 ? c->n0l / c->M : 0);
+  for (int q = 0; q <= K && K > 0; ++q) pb[q] = (int)((long long)q * c->n0l / K);
+  return K;
+}
+
+bool pipeline_ok(const mr_ctx* c, const Plan& plan)
+{
+  int pb[kHeadChunks + 1];
   if (c->comm || c->in_domain || c->profile || c->fast_kind != FK_CHEM ||
-      c->slow_kind != SK_STENCIL || c->imex || K < 3 || plan.ops.size() < 2 ||
-      plan.ops[0].type != Op::SLOW || plan.ops[0].stage != 0 || plan.ops[1].type != Op::CHAIN)
-    return MR_OK;
-  StencilArgs sa = stencil_args(c, c->y_state, c->slots[plan.slot_of[0]], nullptr, nullptr);
-  if (!stencil_plane_ranges(sa)) return MR_OK;
-  int rc = ensure_halo(c);
-  if (rc) return rc;
+      c->slow_kind != SK_STENCIL || c->imex || host_chunks(c, pb) < 3 || plan.ops.size() < 2)
+    return false;
+  return stencil_plane_ranges(stencil_args(c, c->y_state, nullptr, nullptr, nullptr));
+}
+
+int ensure_copy_stream(mr_ctx* c)
+{
   if (!c->copy_stream) {
     MR_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     for (cudaEvent_t& e : c->ev_copy)
       MR_CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  int pb[kHeadChunks + 1];
-  for (int q = 0; q <= K; ++q) pb[q] = (int)((long long)q * c->n0l / K);
-  // the copies start after whatever the compute stream still does with y_state
-  MR_CUDA_TRY(c, cudaEventRecord(c->ev_copy[kHeadChunks], st));
-  MR_CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->ev_copy[kHeadChunks], 0));
-  const size_t pitch = c->ncell * sizeof(double);
-  for (int i = 0; i < K; ++i) {
-    const int q = (i + K - 1) % K;  // K-1, 0, 1, ..., K-2
-    const size_t off = (size_t)pb[q] * c->plane;
-    MR_CUDA_TRY(c, cudaMemcpy2DAsync(c->y_state + off, pitch, hin + off, pitch,
-                                     (size_t)(pb[q + 1] - pb[q]) * c->plane * sizeof(double),
-                                     c->ncomp, cudaMemcpyHostToDevice, c->copy_stream));
-    MR_CUDA_TRY(c, cudaEventRecord(c->ev_copy[q], c->copy_stream));
-  }
-  // periodic ghosts: the first and the last M planes (chunks 0 and K-1)
-  MR_CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_copy[0], 0));
-  MR_CUDA_TRY(c, launch_halo_pack(c->y_state, c->send_lo, c->send_hi, c->ncomp, c->n0l, c->plane,
-                                  M, st));
-  c->launches++;
-  sa.halo_lo = c->send_hi;
-  sa.halo_hi = c->send_lo;
-  const Op& o = plan.ops[1];
-  ChainArgs a;
+  return MR_OK;
+}
+
+void fill_chain_args(mr_ctx* c, const Op& o, const Plan& plan, double t, double H,
+                     const double* yin, ChainArgs& a)
+{
   std::memset(&a, 0, sizeof(a));
   a.nst = (int)o.stages.size();
   a.ndeg = ndeg_of(c);
   for (int q = 0; q < a.nst; ++q) fill_chain_stage(c, o.stages[q], t, H, plan, a.st[q]);
   a.tab = c->tab;
-  a.y_in = c->y_state;
+  a.y_in = yin;
   a.y_out = c->y_work;
   for (int q = 0; q < (int)c->slots.size() && q < MR_MAXSLOT; ++q) a.fE[q] = c->slots[q];
   a.ncell = c->ncell;
   a.ncomp = c->ncomp;
   a.fail = c->d_fail;
-  {
-    const NvtxRange r0("slow f_E", 0, -1);
-    const NvtxRange r1("fast IVP chain", o.stages.front(), o.stages.back());
-    for (int q = 0; q < K; ++q) {
-      // chunks q - 1, q and q + 1 (the ghosts of chunks 0 and K-1 are packed);
-      // the copy stream is in order K-1, 0, 1, ..., K-2, so one event covers
-      // all three: chunk q + 1's, or chunk K-2's for the last two chunks
-      MR_CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_copy[q + 1 <= K - 2 ? q + 1 : K - 2], 0));
-      sa.i_lo = pb[q];
-      sa.i_hi = pb[q + 1];
-      MR_CUDA_TRY(c, launch_stencil(sa, st));
-      a.cell0 = (size_t)pb[q] * c->plane;
-      a.cell1 = (size_t)pb[q + 1] * c->plane;
-      MR_CUDA_TRY(c, launch_chem_chain(ccfg, a, *c->chemP, st));
-      c->launches += 2;
-    }
+}
+
+// chunked copy of planes [pb[q], pb[q+1]) of every component
+cudaError_t copy_chunk(mr_ctx* c, double* dst, const double* src, const int* pb, int q,
+                       cudaMemcpyKind kind)
+{
+  const size_t off = (size_t)pb[q] * c->plane, pitch = c->ncell * sizeof(double);
+  return cudaMemcpy2DAsync(dst + off, pitch, src + off, pitch,
+                           (size_t)(pb[q + 1] - pb[q]) * c->plane * sizeof(double), c->ncomp,
+                           kind, c->copy_stream);
+}
+
+// Upload + ops[0] (SLOW 0) + ops[1] (CHAIN).  Chunks are copied in the order
+// K-1, 0, 1, ..., K-2 (the last chunk holds the periodic ghosts of the
+// first).  *nops = 2 when done, 0 when the plan does not start that way.
+int head_upload(mr_ctx* c, const double* hin, const Plan& plan, double t, double H,
+                const ChemCfg& ccfg, cudaStream_t st, int* nops)
+{
+  *nops = 0;
+  if (plan.ops[0].type != Op::SLOW || plan.ops[0].stage != 0 || plan.ops[1].type != Op::CHAIN)
+    return MR_OK;
+  int pb[kHeadChunks + 1];
+  const int K = host_chunks(c, pb);
+  int rc = ensure_halo(c);
+  if (rc) return rc;
+  rc = ensure_copy_stream(c);
+  if (rc) return rc;
+  // the copies start after whatever the compute stream still does with y_state
+  MR_CUDA_TRY(c, cudaEventRecord(c->ev_copy[kHeadChunks], st));
+  MR_CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->ev_copy[kHeadChunks], 0));
+  for (int i = 0; i < K; ++i) {
+    const int q = (i + K - 1) % K;  // K-1, 0, 1, ..., K-2
+    MR_CUDA_TRY(c, copy_chunk(c, c->y_state, hin, pb, q, cudaMemcpyHostToDevice));
+    MR_CUDA_TRY(c, cudaEventRecord(c->ev_copy[q], c->copy_stream));
+  }
+  // periodic ghosts: the first and the last M planes (chunks 0 and K-1)
+  MR_CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_copy[0], 0));
+  MR_CUDA_TRY(c, launch_halo_pack(c->y_state, c->send_lo, c->send_hi, c->ncomp, c->n0l, c->plane,
+                                  c->M, st));
+  c->launches++;
+  StencilArgs sa = stencil_args(c, c->y_state, c->slots[plan.slot_of[0]], c->send_hi, c->send_lo);
+  const Op& o = plan.ops[1];
+  ChainArgs a;
+  fill_chain_args(c, o, plan, t, H, c->y_state, a);
+  const NvtxRange r0("slow f_E", 0, -1);
+  const NvtxRange r1("fast IVP chain", o.stages.front(), o.stages.back());
+  for (int q = 0; q < K; ++q) {
+    // chunks q - 1, q and q + 1 (the ghosts of chunks 0 and K-1 are packed);
+    // the copy stream is in order K-1, 0, 1, ..., K-2, so one event covers
+    // all three: chunk q + 1's, or chunk K-2's for the last two chunks
+    MR_CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_copy[q + 1 <= K - 2 ? q + 1 : K - 2], 0));
+    sa.i_lo = pb[q];
+    sa.i_hi = pb[q + 1];
+    MR_CUDA_TRY(c, launch_stencil(sa, st));
+    a.cell0 = (size_t)pb[q] * c->plane;
+    a.cell1 = (size_t)pb[q + 1] * c->plane;
+    MR_CUDA_TRY(c, launch_chem_chain(ccfg, a, *c->chemP, st));
+    c->launches += 2;
   }
   *nops = 2;
+  return MR_OK;
+}
+
+// Index of the final UPDATE of a plan ending CHAIN, SLOW(j), UPDATE(s-1)
+// (+ unreferenced COUNT_SLOW), or -1.
+int tail_index(const Plan& plan, size_t first_op)
+{
+  size_t L = plan.ops.size();
+  while (L > 0 && plan.ops[L - 1].type == Op::COUNT_SLOW) --L;
+  if (L < 3 || L - 3 < first_op) return -1;
+  const Op& oc = plan.ops[L - 3];
+  const Op& os = plan.ops[L - 2];
+  const Op& ou = plan.ops[L - 1];
+  if (oc.type != Op::CHAIN || os.type != Op::SLOW || plan.slot_of[os.stage] < 0 ||
+      ou.type != Op::UPDATE)
+    return -1;
+  return (int)(L - 1);
+}
+
+// ops[L-2..L]: the last chain, slow evaluation and explicit update, chunk by
+// chunk, each finished chunk of the result streaming to hout.  Chain chunks in
+// the order K-1, 0, 1, ..., K-2; the stencil of chunk q once the chains of
+// q - 1..q + 1 are done; the (in-place) update of chunk q once the stencils
+// reading its planes (q - 1..q + 1) are done; then its download.
+int tail_download(mr_ctx* c, const Plan& plan, int L, double t, double H, const ChemCfg& ccfg,
+                  const double* yin, double* hout, cudaStream_t st)
+{
+  int pb[kHeadChunks + 1];
+  const int K = host_chunks(c, pb);
+  int rc = ensure_halo(c);
+  if (rc) return rc;
+  const Op& oc = plan.ops[L - 2];
+  const Op& os = plan.ops[L - 1];
+  const Op& ou = plan.ops[L];
+  ChainArgs a;
+  fill_chain_args(c, oc, plan, t, H, yin, a);
+  StencilArgs sa = stencil_args(c, c->y_work, c->slots[plan.slot_of[os.stage]], c->send_hi,
+                                c->send_lo);
+  ChainStageDev sd;
+  fill_chain_stage(c, ou.stage, t, H, plan, sd);
+  const NvtxRange r0("fast IVP chain", oc.stages.front(), oc.stages.back());
+  const NvtxRange r1("slow f_E", os.stage, -1);
+  const NvtxRange r2("explicit update", ou.stage, -1);
+  auto chain = [&](int q) -> int {
+    a.cell0 = (size_t)pb[q] * c->plane;
+    a.cell1 = (size_t)pb[q + 1] * c->plane;
+    MR_CUDA_TRY(c, launch_chem_chain(ccfg, a, *c->chemP, st));
+    c->launches++;
+    return MR_OK;
+  };
+  auto stencil = [&](int q) -> int {
+    sa.i_lo = pb[q];
+    sa.i_hi = pb[q + 1];
+    MR_CUDA_TRY(c, launch_stencil(sa, st));
+    c->launches++;
+    return MR_OK;
+  };
+  auto update_out = [&](int q) -> int {
+    const size_t off = (size_t)pb[q] * c->plane;
+    const double* f[MR_MAXREF];
+    for (int r = 0; r < sd.nref; ++r) f[r] = c->slots[sd.ref_slot[r]] + off;
+    MR_CUDA_TRY(c, launch_update_rows(c->y_work + off, c->y_work + off, sd.nref, f, sd.coef[0],
+                                      (size_t)(pb[q + 1] - pb[q]) * c->plane, c->ncomp, c->ncell,
+                                      ou.stage, c->d_fail, st));
+    c->launches++;
+    MR_CUDA_TRY(c, cudaEventRecord(c->ev_copy[q], st));
+    MR_CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->ev_copy[q], 0));
+    MR_CUDA_TRY(c, copy_chunk(c, hout, c->y_work, pb, q, cudaMemcpyDeviceToHost));
+    return MR_OK;
+  };
+#define MR_TAIL(x)           \
+  do {                       \
+    const int rc_ = (x);     \
+    if (rc_) return rc_;     \
+  } while (0)
+  MR_TAIL(chain(K - 1));
+  MR_TAIL(chain(0));
+  // periodic ghosts of the last slow evaluation: chunks 0 and K-1 are final
+  MR_CUDA_TRY(c, launch_halo_pack(c->y_work, c->send_lo, c->send_hi, c->ncomp, c->n0l, c->plane,
+                                  c->M, st));
+  c->launches++;
+  for (int p = 1; p <= K - 2; ++p) {
+    MR_TAIL(chain(p));
+    MR_TAIL(stencil(p - 1));
+    if (p >= 2) MR_TAIL(update_out(p - 2));
+  }
+  MR_TAIL(stencil(K - 2));
+  MR_TAIL(update_out(K - 3));
+  MR_TAIL(stencil(K - 1));
+  MR_TAIL(update_out(K - 2));
+  MR_TAIL(update_out(K - 1));
+#undef MR_TAIL
   return MR_OK;
 }
 
@@ -1200,12 +1324,17 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
   unsigned long long host_key = MR_NO_FAIL;  // Newton failure (host decision)
 
   NvtxRange step_range("mri_step");
-  size_t first_op = 0;
-  if (n == 1 && c0->host_in) {  // host-buffer step: upload (pipelined when possible)
+  size_t first_op = 0, end_op = plan.ops.size();
+  int tail_L = -1;
+  double* hout = nullptr;
+  if (n == 1 && c0->host_in) {  // host-buffer step: pipelined upload / download
     const double* hin = c0->host_in;
+    hout = c0->host_out;
     c0->host_in = nullptr;
+    c0->host_out = nullptr;
+    const bool pipe = !async && pipeline_ok(c0, plan);
     int nops = 0;
-    if (!async && c0->fast_kind == FK_CHEM) {
+    if (pipe) {
       int rc = head_upload(c0, hin, plan, t, H, ccfg, st, &nops);
       if (rc) return rc;
     }
@@ -1216,8 +1345,24 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
       ycur[0] = c0->y_work;
       first_op = (size_t)nops;
     }
+    if (pipe && hout) tail_L = tail_index(plan, first_op);
+    if (tail_L >= 0) {
+      // the caller's y_out is saved first (behind the upload on the copy
+      // stream): a failing step restores it, so no partial result survives
+      int rc = ensure_copy_stream(c0);
+      if (rc) return rc;
+      if (!c0->y_backup) MR_CUDA_TRY(c0, cudaMalloc(&c0->y_backup, c0->dof * sizeof(double)));
+      if (nops == 0) {
+        MR_CUDA_TRY(c0, cudaEventRecord(c0->ev_copy[kHeadChunks], st));
+        MR_CUDA_TRY(c0, cudaStreamWaitEvent(c0->copy_stream, c0->ev_copy[kHeadChunks], 0));
+      }
+      MR_CUDA_TRY(c0, cudaMemcpyAsync(c0->y_backup, hout, c0->dof * sizeof(double),
+                                      cudaMemcpyHostToDevice, c0->copy_stream));
+      c0->out_streamed = true;
+      end_op = (size_t)tail_L - 2;
+    }
   }
-  for (size_t oi = first_op; oi < plan.ops.size(); ++oi) {
+  for (size_t oi = first_op; oi < end_op; ++oi) {
     const Op& o = plan.ops[oi];
     if (o.type == Op::COUNT_SLOW) continue;
     if (o.type == Op::MISSING) {
@@ -1295,6 +1440,11 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
       }
     }
     if (c0->profile) cudaEventRecord(pool_event(c0, timed.back().second + 1), st);
+  }
+  if (tail_L >= 0 && missing_stage < 0 && host_key == MR_NO_FAIL) {
+    int rc = tail_download(c0, plan, tail_L, t, H, ccfg, ycur[0], hout, st);
+    if (rc) return rc;
+    ycur[0] = c0->y_work;
   }
 
   // combine failure keys (min over slabs / ranks)
@@ -2573,9 +2723,22 @@ int mr_mri_step_host(mr_ctx* c, double t, double H, const double* y_in, double* 
   cudaSetDevice(c->device);
   int rc = ensure_state(c);
   if (rc) return rc;
-  c->host_in = y_in;  // uploaded by the step itself (domain_step / head_upload)
+  // the step itself moves the data (domain_step: head_upload / tail_download)
+  c->host_in = y_in;
+  c->host_out = y_out;
+  c->out_streamed = false;
   rc = mr_mri_step(c, t, H, counters, fail_stage);
   c->host_in = nullptr;
+  c->host_out = nullptr;
+  if (c->out_streamed) {  // y_out was written by the step's last ops
+    c->out_streamed = false;
+    MR_CUDA_TRY(c, cudaStreamSynchronize(c->copy_stream));
+    if (rc) {  // no partial result: the caller's buffer as it was
+      cudaMemcpy(y_out, c->y_backup, c->dof * sizeof(double), cudaMemcpyDeviceToHost);
+      return rc;
+    }
+    return MR_OK;
+  }
   if (rc) return rc;
   MR_CUDA_TRY(c, cudaMemcpyAsync(y_out, c->y_state, c->dof * sizeof(double),
                                  cudaMemcpyDeviceToHost, c->stream));

@@ -471,18 +471,29 @@ def test_host_buffer_step_equals_device_step(name, n):
     assert np.array_equal(y_pageable, ref)
 
 
-def test_host_buffer_step_failure_keeps_input():
+@pytest.mark.parametrize("name,n", [("C3", 16), ("C4", 64)])
+def test_host_buffer_step_failure_keeps_input(name, n):
     """A failing host-buffer step raises the reference's IntegrationError and
-    writes nothing to y_out (no partial result); the device state is the
-    input, as the reference's mri_integrate keeps y on a throw."""
-    ctx, cfg, y0 = gpu_ctx("C3", 16)
-    bad = y0.copy()
-    bad[7] = np.nan
-    y_out = np.full_like(y0, 3.0)
+    leaves y_out as it was (no partial result -- at 64^3 the result streams
+    out during the step's last ops and the saved y_out is put back); the
+    device state is the input, as the reference's mri_integrate keeps y on a
+    throw.  The NaN sits in the last plane chunk (the periodic ghost of the
+    first)."""
+    import torch
+    ctx, cfg, y0 = gpu_ctx(name, n)
+    bad = torch.from_numpy(y0.copy()).pin_memory().numpy()
+    bad[y0.size // (cfg["S"] + 1) - 7] = np.nan
+    y_out = torch.full((y0.size,), 3.0, dtype=torch.float64).pin_memory().numpy()
     with pytest.raises(P.IntegrationError):
         ctx.mri_step_host(0.0, cfg["H"], bad, y_out)
     assert np.all(y_out == 3.0)
     assert np.array_equal(ctx.download(), bad, equal_nan=True)
+    # the context steps on afterwards: a good host step equals the device step
+    y_ok = torch.from_numpy(y0.copy()).pin_memory().numpy()
+    ctx.mri_step_host(0.0, cfg["H"], y_ok, y_out)
+    dev, _, _ = gpu_ctx(name, n)
+    dev.mri_step(0.0, cfg["H"])
+    assert np.array_equal(y_out, dev.download())
 
 
 # ------------------------------------------------------ asynchronous step
