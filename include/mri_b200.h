@@ -163,7 +163,12 @@ int mr_mri_integrate(mr_ctx* ctx, double t0, double tf, double H, uint64_t* coun
  * mr_mri_step_wait: the commit is a host-side buffer swap. */
 int mr_mri_step_async(mr_ctx* ctx, double t, double H, void* stream);
 int mr_mri_step_wait(mr_ctx* ctx, uint64_t* counters, int* fail_stage);
-/* End-to-end variant with HOST buffers: H2D of y_in, the step, D2H of y_out. */
+/* End-to-end variant with HOST buffers: H2D of y_in, the step, D2H of y_out.
+ * Where the plan allows (single slab, chemistry + order-8 stencil, n >= 64)
+ * the copies are pipelined with the step's first and last ops in plane chunks
+ * (pinned buffers overlap; results bitwise equal to mr_mri_step).  On failure
+ * y_out keeps its previous contents (it is saved on the device first and
+ * written back) and the device state is y_in. */
 int mr_mri_step_host(mr_ctx* ctx, double t, double H, const double* y_in, double* y_out,
                      uint64_t* counters, int* fail_stage);
 /* ark_imex_step / ark_imex_integrate (proj/src/mri.cpp:437-557): the
