@@ -15,6 +15,7 @@
 #define MR_MAXCHAIN 6  // cell-local MRI stages fused into one launch
 #define MR_MAXSLOT 24 // stored slow-RHS stage values
 #define MR_MAXLIN 8    // components of the linear test plugins
+#define MR_MAXTAU 1024 // per-evaluation tau values carried by a chain launch
 
 // Explicit Butcher table (butcher.hpp:16-27)
 struct TableDev {
@@ -50,6 +51,11 @@ struct ChainArgs {
   size_t ncell;  // cells of the slab (the stride of a component)
   int ncomp;
   unsigned long long* fail;
+  // tau = (theta - t_start) / span of every inner stage of the chain's FastIvp
+  // stages in evaluation order (uniform scalars computed once on the host
+  // with the same IEEE operations; ntau = 0: the kernel computes them)
+  int ntau;
+  double tau[MR_MAXTAU];
   size_t cell0, cell1;  // cells [cell0, cell1) this launch advances (chemistry
                         // chain; cell1 == 0: all), e.g. the plane chunks of a
                         // host-buffer step whose upload is still in flight

@@ -212,7 +212,10 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
     m.part[(0 * NW + w) * 32 + c] = p0;
     m.part[(1 * NW + w) * 32 + c] = p1;
     m.part[(2 * NW + w) * 32 + c] = p2;
-    m.part[(3 * NW + w) * 32 + c] = e;
+    // the energy has one owner: one row, not a sum over the warps
+#pragma unroll
+    for (int t = 0; t < SPL; ++t)
+      if (kk[t] == S) m.part[(3 * NW) * 32 + c] = e;
   }
   __syncthreads();
   MR_PH(1);  // energy partial sums
@@ -223,8 +226,8 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
       E0 += m.part[(0 * NW + q) * 32 + c];
       E1 += m.part[(1 * NW + q) * 32 + c];
       E2 += m.part[(2 * NW + q) * 32 + c];
-      ee += m.part[(3 * NW + q) * 32 + c];
     }
+    ee = m.part[(3 * NW) * 32 + c];
     const double de = ee - E0;
     const double T = (2.0 * de) / (E1 + sqrt(E1 * E1 + 4.0 * E2 * de));
     m.tinf[0 * 32 + c] = T;
@@ -371,6 +374,7 @@ __global__ void __launch_bounds__(NW * 32, chem_min_blocks(NW, NDEG))
     y[t] = (active && k < ncomp) ? a.y_in[(size_t)k * nc + cell] : 0.0;
   }
   bool failed = !active;
+  int ev = 0;  // evaluation index (uniform): into a.tau
 
   for (int si = 0; si < a.nst; ++si) {
     const ChainStageDev& st = a.st[si];
@@ -454,8 +458,14 @@ __global__ void __launch_bounds__(NW * 32, chem_min_blocks(NW, NDEG))
             failed = true;
           }
         }
-        const double theta = dadd(t0, dmul(a.tab.c[j], h));
-        const double tau = __ddiv_rn(dadd(theta, -st.t_start), st.span);
+        double tau;
+        if (ev < a.ntau) {
+          tau = a.tau[ev];
+        } else {
+          const double theta = dadd(t0, dmul(a.tab.c[j], h));
+          tau = __ddiv_rn(dadd(theta, -st.t_start), st.span);
+        }
+        ++ev;
         double f[SPL];
         chem_block_eval<NW, SPL>(P, m, w, c, kk, stg, f MR_PH_PASS);
         const double hb = dmul(h, a.tab.b[j]);

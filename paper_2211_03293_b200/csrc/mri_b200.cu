@@ -583,6 +583,28 @@ void fill_chain_stage(const mr_ctx* c, int i, double t, double H, const Plan& p,
   }
 }
 
+// Per-evaluation tau of a chain's FastIvp stages, in the kernels' evaluation
+// order and with their operations (dadd/dmul/ddiv in IEEE double: the host
+// values are bitwise the device's); too many evaluations: ntau = 0.
+void fill_chain_taus(const mr_ctx* c, ChainArgs& a)
+{
+  a.ntau = 0;
+  int e = 0;
+  for (int si = 0; si < a.nst; ++si) {
+    const ChainStageDev& st = a.st[si];
+    if (st.kind != 0) continue;
+    if (e + st.n_sub * c->tab.s > MR_MAXTAU) return;
+    for (int sub = 0; sub < st.n_sub; ++sub) {
+      const double t0 = st.t_start + (double)sub * st.h_sub;
+      for (int j = 0; j < c->tab.s; ++j) {
+        const double theta = t0 + c->tab.c[j] * st.h_sub;
+        a.tau[e++] = (theta + -st.t_start) / st.span;
+      }
+    }
+  }
+  a.ntau = e;
+}
+
 cudaEvent_t pool_event(mr_ctx* c, size_t idx)
 {
   while (c->ev_pool.size() <= idx) {
@@ -1108,6 +1130,7 @@ void fill_chain_args(mr_ctx* c, const Op& o, const Plan& plan, double t, double 
   a.ncell = c->ncell;
   a.ncomp = c->ncomp;
   a.fail = c->d_fail;
+  fill_chain_taus(c, a);
 }
 
 // chunked copy of planes [pb[q], pb[q+1]) of every component
@@ -1430,6 +1453,7 @@ int domain_step(mr_ctx** cs, int n, double t, double H, uint64_t* counters, int*
         a.ncell = c->ncell;
         a.ncomp = c->ncomp;
         a.fail = c->d_fail;
+        if (c->fast_kind == FK_CHEM) fill_chain_taus(c, a);
         sdev(c);
         if (c->fast_kind == FK_CHEM)
           MR_CUDA_TRY(c, launch_chem_chain(ccfg, a, *c->chemP, sst(c, st)));
