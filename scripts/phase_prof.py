@@ -12,8 +12,13 @@ import paper_2211_03293_b200 as P
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C4"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+R = int(sys.argv[3]) if len(sys.argv) > 3 else None  # optional reaction-count override
 ctx = P.Context(0)
-cfg, y0 = P.setup_workload(ctx, name, n=n)
+from paper_2211_03293_b200.configs import CONFIGS
+config = dict(CONFIGS[name])
+if R:
+    config["R"] = R
+cfg, y0 = P.setup_workload(ctx, name, n=n, config=config)
 L = P.lib()
 f = L.mr_debug_chem_phases
 f.restype = C.c_int
@@ -29,7 +34,7 @@ evals = int(cnt[0]) // 1  # per cell
 names = ["rk bookkeeping / wait", "energy partials + barrier", "temperature (warp 0)",
          "species rows", "reactions", "production (warp 0)", "kernel total"]
 tot_phase = v[:6].sum()
-print(f"{name} n={n}: grid blocks={blocks:.0f}, block launches={v[7]:.0f}, fast evals/cell/step={evals}")
+print(f"{name} n={n} R={cfg['R']}: grid blocks={blocks:.0f}, block launches={v[7]:.0f}, fast evals/cell/step={evals}")
 for i, nm in enumerate(names):
     per = v[i] / blocks / max(evals, 1)
     share = v[i] / v[6] if i < 6 else 1.0
