@@ -469,6 +469,9 @@ def test_host_buffer_step_equals_device_step(name, n):
     y_pageable = np.zeros_like(y0)  # pageable destination: same result
     host.mri_step_host(0.0, cfg["H"], y0, y_pageable)
     assert np.array_equal(y_pageable, ref)
+    y_inplace = torch.from_numpy(y0.copy()).pin_memory().numpy()  # y_in is y_out
+    host.mri_step_host(0.0, cfg["H"], y_inplace, y_inplace)
+    assert np.array_equal(y_inplace, ref)
 
 
 @pytest.mark.parametrize("name,n", [("C3", 16), ("C4", 64)])
