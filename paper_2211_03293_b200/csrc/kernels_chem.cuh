@@ -104,10 +104,11 @@ __device__ __forceinline__ void mr_exp_pair(double x, double& e, double& ei)
 //   tinf double  [3][32]    T, lnT, 1/T
 //   spc  double  [S1][10]   per-species constants {c0,c1 | c2,h0 | a,hb | s0,rhoW | Wrho,-}
 //                            (warp-uniform broadcast LDS.128 instead of indexed LDC)
+//   lsh  ushort4 [S1][MAXCHUNK] production-list headers (ditto)
 __host__ __device__ inline size_t smem_bytes(int NW, int S1, int rc, int blob_words)
 {
   return (size_t)S1 * 512 + (size_t)S1 * 256 + (size_t)rc * 256 + 256 + (size_t)blob_words * 16 +
-         (size_t)4 * NW * 256 + 3 * 256 + (size_t)S1 * 80;
+         (size_t)4 * NW * 256 + 3 * 256 + (size_t)S1 * 80 + (size_t)S1 * MR_CHEM_MAXCHUNK * 8;
 }
 
 struct Smem {
@@ -119,6 +120,7 @@ struct Smem {
   double* part;
   double* tinf;
   const double2* spc;  // [S1][5] double2
+  const ushort4* lsh;   // [S1][MR_CHEM_MAXCHUNK]
 };
 
 // carves shared memory and stages the mechanism blob (all threads; ends with
@@ -138,6 +140,10 @@ __device__ __forceinline__ Smem stage(char* base, const ChemParams& P, int NW, i
   m.tinf = m.part + 4 * NW * 32;
   double2* spc = reinterpret_cast<double2*>(m.tinf + 3 * 32);
   m.spc = spc;
+  ushort4* lsh = reinterpret_cast<ushort4*>(spc + S1 * 5);
+  m.lsh = lsh;
+  for (int i = threadIdx.x; i < P.S * MR_CHEM_MAXCHUNK; i += blockDim.x)
+    lsh[i] = P.lst[i / MR_CHEM_MAXCHUNK][i % MR_CHEM_MAXCHUNK];
   for (int i = threadIdx.x; i < P.S; i += blockDim.x) {
     spc[i * 5 + 0] = make_double2(P.c0[i], P.c1[i]);
     spc[i * 5 + 1] = make_double2(P.c2[i], P.h0[i]);
@@ -310,7 +316,7 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
     for (int t = 0; t < SPL; ++t) {
       const int k = kk[t];
       if (k < S) {
-        const ushort4 L = P.lst[k][ch];
+        const ushort4 L = m.lsh[k * MR_CHEM_MAXCHUNK + ch];
         double s_ = acc[t];
         for (int i = 0; i < L.y; ++i) {
           const uint4 e = m.ent[L.x + i];
