@@ -195,6 +195,41 @@ int mr_reference_solution(mr_ctx* ctx, double t0, double tf, double h_ref, int* 
 int mr_erk_integrate(mr_ctx* ctx, int s, const double* A, const double* b, const double* c,
                      double t0, double tf, double h, uint64_t* n_explicit_evals,
                      int* fail_stage);
+
+/* Spectral deferred corrections on the device plugins (proj/src/sdc.cpp).
+ * mr_sdc_integrate: sdc_integrate (sdc.cpp:267-281) of sum_rhs with an
+ *   n-node rule -- nodes[n] on [0,1] and the integration matrix S[(n-1)*n]
+ *   of lobatto_nodes(n) (sdc.hpp:17-27) -- and n_sweeps correction sweeps;
+ *   evaluations counted into *n_evals like harness.cpp:356-366.
+ * mr_mrsdc_load + mr_mrsdc_integrate: mrsdc_integrate (sdc.cpp:283-301) with
+ *   the scheme of build_scheme(X, Y, Z, n_sweeps) (sdc.hpp:29-55) flattened:
+ *   coarse_nodes[X], fine_nodes[n_fine], coarse_of_fine[n_fine],
+ *   coarse_index_of_fine[n_fine] (-1: no coarse node), fine_row[(n_fine-1)*Y],
+ *   application_offset[n_fine-1], coarse_row[(n_fine-1)*X]; counters
+ *   (EvalCounters order) accumulate n_fast_evals / n_explicit_evals.
+ * A non-finite node update fails with MR_INTEGRATION, fail_stage = the node
+ * (the reference's IntegrationError stage_index), the state restored to the
+ * call's input and the counters as far as the reference had counted.  The
+ * node caches need 2 n_fine + 2 X + 5 state-sized buffers (MR_CUDA when the
+ * device runs out of memory). */
+int mr_sdc_integrate(mr_ctx* ctx, int n_nodes, const double* nodes, const double* S, int n_sweeps,
+                     double t0, double tf, double H, uint64_t* n_evals, int* fail_stage);
+int mr_mrsdc_load(mr_ctx* ctx, int X, int Y, int n_fine, int n_sweeps, const double* coarse_nodes,
+                  const double* fine_nodes, const int* coarse_of_fine,
+                  const int* coarse_index_of_fine, const double* fine_row,
+                  const int* application_offset, const double* coarse_row);
+int mr_mrsdc_integrate(mr_ctx* ctx, double t0, double tf, double H, uint64_t* counters,
+                       int* fail_stage);
+/* The reference's node sets, built on the host with its arithmetic (bitwise
+ * equal): lobatto_nodes(n) (sdc.cpp:60-80; nodes[n], S[(n-1)*n]) and
+ * build_scheme(X, Y, Z, .) (sdc.cpp:82-153; *n_fine = capacity in / count
+ * out, all array pointers NULL = size query).  mr_mrsdc_build = build_scheme
+ * + mr_mrsdc_load.  No device work: callable without a GPU. */
+int mr_lobatto_rule(int n, double* nodes, double* S);
+int mr_mrsdc_scheme(int X, int Y, int Z, int* n_fine, double* coarse_nodes, double* fine_nodes,
+                    int* coarse_of_fine, int* coarse_index_of_fine, double* fine_row,
+                    int* application_offset, double* coarse_row);
+int mr_mrsdc_build(mr_ctx* ctx, int X, int Y, int Z, int n_sweeps);
 /* Location of the last failure: MRI stage, fast substep, inner stage. */
 int mr_last_failure(const mr_ctx* ctx, int* mri_stage, int* substep, int* inner_stage);
 

@@ -148,6 +148,14 @@ def ref():
                                                  _dp, _ip, C.c_char_p, C.c_size_t]
         L.ref_sys_erk_integrate.argtypes = [C.c_void_p, C.c_char_p, C.c_double, C.c_double,
                                             C.c_double, _dp, _u64p, _ip, C.c_char_p, C.c_size_t]
+        L.ref_lobatto_nodes.argtypes = [C.c_int, _dp, _dp, C.c_char_p, C.c_size_t]
+        L.ref_mrsdc_scheme.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _dp, _dp, _ip, _ip,
+                                       _dp, _ip, _dp, C.c_char_p, C.c_size_t]
+        L.ref_sys_sdc_integrate.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double,
+                                            C.c_double, _dp, _u64p, _ip, C.c_char_p, C.c_size_t]
+        L.ref_sys_mrsdc_integrate.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                              C.c_double, C.c_double, C.c_double, _dp, _u64p, _ip,
+                                              C.c_char_p, C.c_size_t]
         L.ref_sys_mri_integrate.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int,
                                             C.c_double, C.c_double, C.c_double, _dp, _u64p, _ip,
                                             C.c_char_p, C.c_size_t]
@@ -317,6 +325,29 @@ class System:
             raise StepError(rc, stage, err, cnt)
         return y2, cnt
 
+    def sdc_integrate(self, n_nodes, sweeps, t0, tf, H, y):
+        """The reference's own sdc_integrate (sdc.cpp:267-281) of sum_rhs with
+        lobatto_nodes(n_nodes); returns (y, evaluations)."""
+        y2 = np.array(y, dtype=np.float64, copy=True)
+        ev = np.zeros(1, dtype=np.uint64)
+        stage = C.c_int(-1)
+        err = C.create_string_buffer(512)
+        rc = ref().ref_sys_sdc_integrate(self.h, n_nodes, sweeps, t0, tf, H, _ptr(y2),
+                                         ev.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(stage),
+                                         err, 512)
+        if rc:
+            raise StepError(rc, stage.value, err.value.decode(), ev)
+        return y2, int(ev[0])
+
+    def mrsdc_integrate(self, X, Y, Z, sweeps, t0, tf, H, y, counters=None):
+        """The reference's own mrsdc_integrate (sdc.cpp:283-301) with
+        build_scheme(X, Y, Z, sweeps)."""
+        rc, y2, cnt, stage, err = self._call(ref().ref_sys_mrsdc_integrate, X, Y, Z, sweeps, t0,
+                                             tf, H, y=y, counters=counters)
+        if rc:
+            raise StepError(rc, stage, err, cnt)
+        return y2, cnt
+
     def erk_integrate(self, table, t0, tf, h, y, use_reference=False):
         """erk_integrate (erk.cpp:40-57) of the summed RHS with a registered
         table; returns (y, stage evaluations)."""
@@ -407,3 +438,37 @@ def norms():
             return bool(L.orc_all_finite(px, x.size))
 
     return N
+
+
+def ref_lobatto_nodes(n):
+    """The reference's lobatto_nodes(n) (sdc.cpp:60-80): (nodes, S flattened)."""
+    nodes = np.zeros(n)
+    S = np.zeros((n - 1) * n)
+    err = C.create_string_buffer(256)
+    if ref().ref_lobatto_nodes(n, _ptr(nodes), _ptr(S), err, 256):
+        raise ValueError(err.value.decode())
+    return nodes, S
+
+
+def ref_mrsdc_scheme(X, Y, Z, sweeps=1):
+    """The reference's build_scheme (sdc.cpp:82-153), flattened like
+    paper_2211_03293_b200.mrsdc_scheme."""
+    nf = C.c_int(0)
+    err = C.create_string_buffer(256)
+    if ref().ref_mrsdc_scheme(X, Y, Z, sweeps, C.byref(nf), None, None, None, None, None, None,
+                              None, err, 256):
+        raise ValueError(err.value.decode())
+    n = nf.value
+    sc = dict(X=X, Y=Y, n_fine=n, coarse_nodes=np.zeros(X), fine_nodes=np.zeros(n),
+              coarse_of_fine=np.zeros(n, dtype=np.int32),
+              coarse_index_of_fine=np.zeros(n, dtype=np.int32),
+              fine_row=np.zeros((n - 1) * Y), application_offset=np.zeros(n - 1, dtype=np.int32),
+              coarse_row=np.zeros((n - 1) * X))
+    ip = C.POINTER(C.c_int)
+    if ref().ref_mrsdc_scheme(X, Y, Z, sweeps, C.byref(nf), _ptr(sc["coarse_nodes"]),
+                              _ptr(sc["fine_nodes"]), sc["coarse_of_fine"].ctypes.data_as(ip),
+                              sc["coarse_index_of_fine"].ctypes.data_as(ip), _ptr(sc["fine_row"]),
+                              sc["application_offset"].ctypes.data_as(ip), _ptr(sc["coarse_row"]),
+                              err, 256):
+        raise ValueError(err.value.decode())
+    return sc

@@ -18,6 +18,7 @@
 #include "multirate/butcher.hpp"
 #include "multirate/erk.hpp"
 #include "multirate/mri.hpp"
+#include "multirate/sdc.hpp"
 
 extern "C" {
 #include "mri_oracle.h"
@@ -316,6 +317,80 @@ extern "C" int ref_sys_ark_imex_integrate(orc_sys* sys, double t0, double tf, do
     ImplicitStageSolver solver = stage_solver(sys, yv);
     const ArkPair pair = lookup_ark_pair("ark436-imex-pair");
     StateVector out = ark_imex_integrate(pair, ps, solver, t0, tf, H, yv, c);
+    std::memcpy(y, out.data(), sizeof(double) * ps.dimension);
+  });
+  counters_to(c, counters);
+  return rc;
+}
+
+// lobatto_nodes(n) (sdc.cpp:60-80): nodes[n], S[(n-1)*n]
+extern "C" int ref_lobatto_nodes(int n, double* nodes, double* S, char* err, size_t errlen)
+{
+  return guarded(err, errlen, nullptr, [&] {
+    const QuadratureNodes q = lobatto_nodes(n);
+    for (int i = 0; i < n; ++i) nodes[i] = q.nodes[i];
+    for (int i = 0; i + 1 < n; ++i)
+      for (int j = 0; j < n; ++j) S[i * n + j] = q.S[i][j];
+  });
+}
+
+// build_scheme(X, Y, Z, sweeps) (sdc.cpp:82-153), flattened like mr_mrsdc_scheme
+extern "C" int ref_mrsdc_scheme(int X, int Y, int Z, int sweeps, int* n_fine, double* coarse_nodes,
+                                double* fine_nodes, int* coarse_of_fine, int* coarse_index_of_fine,
+                                double* fine_row, int* application_offset, double* coarse_row,
+                                char* err, size_t errlen)
+{
+  return guarded(err, errlen, nullptr, [&] {
+    const MrsdcScheme s = build_scheme(X, Y, Z, sweeps);
+    const int cap = *n_fine;
+    *n_fine = s.n_fine;
+    if (!coarse_nodes || cap < s.n_fine) return;
+    for (int j = 0; j < X; ++j) coarse_nodes[j] = s.coarse.nodes[j];
+    for (int q = 0; q < s.n_fine; ++q) {
+      fine_nodes[q] = s.fine_nodes[q];
+      coarse_of_fine[q] = s.coarse_of_fine[q];
+      coarse_index_of_fine[q] = s.coarse_index_of_fine[q];
+    }
+    for (int q = 0; q + 1 < s.n_fine; ++q) {
+      for (int j = 0; j < Y; ++j) fine_row[q * Y + j] = s.fine_row[q][j];
+      application_offset[q] = s.application_offset[q];
+      for (int j = 0; j < X; ++j) coarse_row[q * X + j] = s.coarse_row[q][j];
+    }
+  });
+}
+
+// sdc_integrate (sdc.cpp:267-281) of sum_rhs with lobatto_nodes(n), counting
+// into *evals like harness.cpp:356-366
+extern "C" int ref_sys_sdc_integrate(orc_sys* sys, int n, int sweeps, double t0, double tf,
+                                     double H, double* y, uint64_t* evals, int* fail_stage,
+                                     char* err, size_t errlen)
+{
+  std::size_t cnt = 0;
+  const int rc = guarded(err, errlen, fail_stage, [&] {
+    PartitionedSystem ps = make_system(sys);
+    StateVector yv(ps.dimension);
+    std::memcpy(yv.data(), y, sizeof(double) * ps.dimension);
+    const QuadratureNodes nodes = lobatto_nodes(n);
+    RhsFn f = [&ps](double t, const StateVector& v) { return ps.sum_rhs(t, v); };
+    StateVector out = sdc_integrate(nodes, f, t0, tf, H, yv, sweeps, &cnt);
+    std::memcpy(y, out.data(), sizeof(double) * ps.dimension);
+  });
+  *evals += cnt;
+  return rc;
+}
+
+// mrsdc_integrate (sdc.cpp:283-301) with build_scheme(X, Y, Z, sweeps)
+extern "C" int ref_sys_mrsdc_integrate(orc_sys* sys, int X, int Y, int Z, int sweeps, double t0,
+                                       double tf, double H, double* y, uint64_t* counters,
+                                       int* fail_stage, char* err, size_t errlen)
+{
+  EvalCounters c = counters_from(counters);
+  const int rc = guarded(err, errlen, fail_stage, [&] {
+    PartitionedSystem ps = make_system(sys);
+    StateVector yv(ps.dimension);
+    std::memcpy(yv.data(), y, sizeof(double) * ps.dimension);
+    const MrsdcScheme scheme = build_scheme(X, Y, Z, sweeps);
+    StateVector out = mrsdc_integrate(scheme, ps, t0, tf, H, yv, c);
     std::memcpy(y, out.data(), sizeof(double) * ps.dimension);
   });
   counters_to(c, counters);

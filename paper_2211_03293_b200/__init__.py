@@ -100,6 +100,15 @@ def lib():
                                        C.c_double, _u64p, _ip]),
         "mr_ark_imex_step": (C.c_int, [vp, C.c_double, C.c_double, _u64p, _ip]),
         "mr_ark_imex_integrate": (C.c_int, [vp, C.c_double, C.c_double, C.c_double, _u64p, _ip]),
+        "mr_sdc_integrate": (C.c_int, [vp, C.c_int, _dp, _dp, C.c_int, C.c_double, C.c_double,
+                                       C.c_double, _u64p, _ip]),
+        "mr_mrsdc_load": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _ip, _ip,
+                                    _dp, _ip, _dp]),
+        "mr_mrsdc_build": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int]),
+        "mr_mrsdc_integrate": (C.c_int, [vp, C.c_double, C.c_double, C.c_double, _u64p, _ip]),
+        "mr_lobatto_rule": (C.c_int, [C.c_int, _dp, _dp]),
+        "mr_mrsdc_scheme": (C.c_int, [C.c_int, C.c_int, C.c_int, _ip, _dp, _dp, _ip, _ip, _dp, _ip,
+                                      _dp]),
         "mr_state_upload": (C.c_int, [vp, _dp]),
         "mr_state_download": (C.c_int, [vp, _dp]),
         "mr_state_device_ptr": (C.c_void_p, [vp]),
@@ -152,6 +161,37 @@ def _p(a, t=_dp):
 # --------------------------------------------------------------------------
 # host-side generators (product implementation, C++)
 # --------------------------------------------------------------------------
+def lobatto_rule(n: int):
+    """lobatto_nodes(n) (sdc.cpp:60-80): (nodes[n], S[(n-1) x n] flattened),
+    built by the library with the reference's arithmetic (no GPU needed)."""
+    nodes = np.zeros(n, dtype=np.float64)
+    S = np.zeros(max(n - 1, 0) * n, dtype=np.float64)
+    if lib().mr_lobatto_rule(n, _p(nodes), _p(S)):
+        raise ContractError("lobatto_nodes: only n = 3 or 5 supported")
+    return nodes, S
+
+
+def mrsdc_scheme(X: int, Y: int, Z: int):
+    """build_scheme(X, Y, Z, .) (sdc.cpp:82-153) flattened: the arrays
+    mr_mrsdc_load takes (no GPU needed)."""
+    nf = C.c_int(0)
+    if lib().mr_mrsdc_scheme(X, Y, Z, C.byref(nf), None, None, None, None, None, None, None):
+        raise ContractError("build_scheme: need X,Y in {3,5}, Z >= 1")
+    n = nf.value
+    sc = dict(X=X, Y=Y, n_fine=n, coarse_nodes=np.zeros(X), fine_nodes=np.zeros(n),
+              coarse_of_fine=np.zeros(n, dtype=np.int32),
+              coarse_index_of_fine=np.zeros(n, dtype=np.int32),
+              fine_row=np.zeros((n - 1) * Y), application_offset=np.zeros(n - 1, dtype=np.int32),
+              coarse_row=np.zeros((n - 1) * X))
+    rc = lib().mr_mrsdc_scheme(X, Y, Z, C.byref(nf), _p(sc["coarse_nodes"]), _p(sc["fine_nodes"]),
+                               _p(sc["coarse_of_fine"], _ip), _p(sc["coarse_index_of_fine"], _ip),
+                               _p(sc["fine_row"]), _p(sc["application_offset"], _ip),
+                               _p(sc["coarse_row"]))
+    if rc:
+        raise ContractError("build_scheme failed")
+    return sc
+
+
 def mechanism(seed: int, S: int, R: int):
     sp = np.zeros(5 * S)
     rx = np.zeros(3 * R)
@@ -446,6 +486,45 @@ class Context:
         rc = self.L.mr_erk_integrate(self.h, len(b), _p(A), _p(b), _p(c), t0, tf, h,
                                      _p(ev, _u64p), C.byref(stage))
         cnt[2] += ev[0]
+        self._check(rc, stage.value)
+        return cnt
+
+    # ---- spectral deferred corrections (proj/src/sdc.cpp) -------------------
+    def sdc_integrate(self, n_nodes, sweeps, t0, tf, H, counters=None):
+        """sdc_integrate (sdc.cpp:267-281) of f_fast + f_implicit + f_explicit
+        with lobatto_nodes(n_nodes) and `sweeps` correction sweeps: the
+        harness's sdc family; evaluations into counters[MR_CNT_EXPLICIT_EVALS]
+        (harness.cpp:356-366)."""
+        nodes, S = lobatto_rule(n_nodes)
+        cnt = self.counters() if counters is None else counters
+        ev = np.zeros(1, dtype=np.uint64)
+        stage = C.c_int(-1)
+        rc = self.L.mr_sdc_integrate(self.h, n_nodes, _p(nodes), _p(S), sweeps, t0, tf, H,
+                                     _p(ev, _u64p), C.byref(stage))
+        cnt[2] += ev[0]
+        self._check(rc, stage.value)
+        return cnt
+
+    def mrsdc_build(self, X, Y, Z, sweeps):
+        """build_scheme(X, Y, Z, sweeps) (sdc.cpp:82-153) for mrsdc_integrate."""
+        self._check(self.L.mr_mrsdc_build(self.h, X, Y, Z, sweeps))
+
+    def mrsdc_load(self, scheme, sweeps):
+        """Load a flattened MRSDC scheme (mrsdc_scheme(), or the reference's
+        build_scheme) for mrsdc_integrate."""
+        sc = {k: np.ascontiguousarray(v) for k, v in scheme.items() if k not in ("X", "Y", "n_fine")}
+        self._check(self.L.mr_mrsdc_load(
+            self.h, scheme["X"], scheme["Y"], scheme["n_fine"], sweeps,
+            _p(sc["coarse_nodes"]), _p(sc["fine_nodes"]), _p(sc["coarse_of_fine"], _ip),
+            _p(sc["coarse_index_of_fine"], _ip), _p(sc["fine_row"]),
+            _p(sc["application_offset"], _ip), _p(sc["coarse_row"])))
+
+    def mrsdc_integrate(self, t0, tf, H, counters=None):
+        """mrsdc_integrate (sdc.cpp:283-301) of the loaded scheme: the harness's
+        mrsdc-XYZ family."""
+        cnt = self.counters() if counters is None else counters
+        stage = C.c_int(-1)
+        rc = self.L.mr_mrsdc_integrate(self.h, t0, tf, H, _p(cnt, _u64p), C.byref(stage))
         self._check(rc, stage.value)
         return cnt
 

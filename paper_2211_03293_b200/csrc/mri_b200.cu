@@ -195,6 +195,13 @@ struct mr_ctx {
   double* cg_gather = nullptr;  // [nranks] for the cross-rank fixed-order sum
   double* newton_w = nullptr;   // ImplicitStageSolver::weights (local slab); null = unit
   std::vector<double*> rs_bufs;  // reference solution: k[6], stage, f_fast, f_implicit
+  std::vector<double*> sdc_bufs; // (multirate) SDC: caches, node states, scratch, backup
+  struct SdcScheme {             // mr_mrsdc_load: the reference's MrsdcScheme, flattened
+    bool loaded = false;
+    int X = 0, Y = 0, n_fine = 0, n_sweeps = 0;
+    std::vector<double> coarse_nodes, fine_nodes, fine_row, coarse_row;
+    std::vector<int> coarse_of_fine, coarse_index_of_fine, application_offset;
+  } mrsdc;
   std::vector<double*> ark_bufs; // ARK-IMEX: fE[6], fI[6], f_fast
   double newton_tol = 1.0e-10;  // NewtonConfig defaults (solvers.hpp:19-23)
   double newton_safety = 0.1;
@@ -340,6 +347,8 @@ void free_state(mr_ctx* c)
   free_dev_t(c->newton_w);  // weights are per grid
   for (auto& p : c->rs_bufs) free_dev_t(p);
   c->rs_bufs.clear();
+  for (auto& p : c->sdc_bufs) free_dev_t(p);
+  c->sdc_bufs.clear();
   for (auto& p : c->ark_bufs) free_dev_t(p);
   c->ark_bufs.clear();
   c->halo_elems = 0;
@@ -2983,6 +2992,521 @@ int mr_erk_integrate(mr_ctx* c, int s, const double* A, const double* b, const d
     return domain_rc(c, erk_integrate_dev(c->slabs.data(), (int)c->slabs.size(), s, A, b, t0, tf,
                                           h, n_explicit_evals, fail_stage));
   return erk_integrate_dev(&c, 1, s, A, b, t0, tf, h, n_explicit_evals, fail_stage);
+}
+
+// ---- spectral deferred corrections (proj/src/sdc.cpp) ----
+// One engine for both of the reference's SDC drivers:
+//   * multirate (mrsdc_step, sdc.cpp:233-265, sweep :155-199): f_fast cached at
+//     the n_fine fine nodes, slow_rhs = f_implicit + f_explicit at the X coarse
+//     nodes, each sweep a forward-Euler correction node by node;
+//   * single rate (sdc_step, :201-231): the same sweep with X = 0, one rule
+//     (fine_row = the integration matrix S, offset 0) and f_total = sum_rhs in
+//     the fine-node cache.
+// Per node the update is one fused multi-operand axpy in the reference's
+// order (quadrature of the previous iterate, fine then coarse, then the four
+// forward-Euler terms), its finite check keyed (sweep, node) so the first
+// failure in execution order is the one reported.  The plugins are autonomous
+// (no t dependence), so the initial caches -- the same state at every node --
+// are evaluated once and copied; they are counted like the reference's
+// separate evaluations.  Cache slots are pointer-swapped between sweeps (the
+// reference copies the k-th iterate's caches).
+namespace {
+struct SdcRun {
+  bool single;  // sdc_step on sum_rhs
+  int X, Y, nf, sweeps;
+  const double *coarse_nodes, *fine_nodes, *fine_row, *coarse_row;
+  const int *coarse_of_fine, *coarse_index_of_fine, *application_offset;
+};
+}  // namespace
+
+static int sdc_integrate_dev(mr_ctx** cs, int n, const SdcRun& R, double t0, double tf, double H,
+                             uint64_t* cnt_fast, uint64_t* cnt_slow, int* fail_stage)
+{
+  if (fail_stage) *fail_stage = -1;
+  mr_ctx* c0 = cs[0];
+  const char* who = R.single ? "sdc_integrate" : "mrsdc_integrate";
+  if (!c0->has_grid) return set_err(c0, MR_CONTRACT, "grid not set (mr_grid_set)");
+  if (c0->fast_kind < 0 || c0->slow_kind < 0)
+    return set_err(c0, MR_CONTRACT, "PartitionedSystem: fast/slow plugins not configured");
+  if (!(tf > t0)) return set_err(c0, MR_CONTRACT, std::string(who) + ": tf must exceed t0");
+  if (!(H > 0.0)) return set_err(c0, MR_CONTRACT, std::string(who) + ": H must be positive");
+  const int nf = R.nf, X = R.single ? 0 : R.X;
+  const int nbuf = 2 * nf + 2 * X + 5;  // f caches x2, slow caches x2, node states x2, scratch x2, backup
+  for (int r = 0; r < n; ++r) {
+    mr_ctx* c = cs[r];
+    if (c->slow_kind == SK_STENCIL && c->n0l < c->M)
+      return set_err(c0, MR_CONTRACT, "slab thinner than the stencil ghost width");
+    cudaSetDevice(c->device);
+    int rc = ensure_state(c);
+    if (rc) return rc;
+    while ((int)c->sdc_bufs.size() < nbuf) {
+      double* p = nullptr;
+      if (cudaMalloc(&p, c->dof * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(c0, MR_CUDA, std::string(who) + ": device memory for the " +
+                                        std::to_string(nbuf) + " node caches exhausted");
+      }
+      c->sdc_bufs.push_back(p);
+    }
+  }
+  const bool fast = c0->fast_kind != FK_NONE, slow = c0->slow_kind != SK_NONE;
+  const bool imp = c0->slow_kind == SK_STENCIL && c0->imex;
+  cudaStream_t st = c0->stream;
+  // per slab: cache pointers (cur / spare) into sdc_bufs
+  std::vector<std::vector<double*>> fcur(n), fspare(n), scur(n), sspare(n);
+  for (int r = 0; r < n; ++r) {
+    auto& B = cs[r]->sdc_bufs;
+    for (int q = 0; q < nf; ++q) {
+      fcur[r].push_back(B[q]);
+      fspare[r].push_back(B[nf + q]);
+    }
+    for (int p = 0; p < X; ++p) {
+      scur[r].push_back(B[2 * nf + p]);
+      sspare[r].push_back(B[2 * nf + X + p]);
+    }
+  }
+  auto node = [&](int r, int q) -> double* {  // state of fine node q >= 1
+    return cs[r]->sdc_bufs[2 * nf + 2 * X + (q & 1)];
+  };
+  auto scrF = [&](int r) { return cs[r]->sdc_bufs[2 * nf + 2 * X + 2]; };
+  auto scrI = [&](int r) { return cs[r]->sdc_bufs[2 * nf + 2 * X + 3]; };
+  auto backup = [&](int r) { return cs[r]->sdc_bufs[2 * nf + 2 * X + 4]; };
+  std::vector<const double*> yc(n);
+  std::vector<double*> oc(n);
+  // f_total (sum_rhs order: fast, implicit, explicit) or the fast part alone
+  auto eval_fine = [&](const std::vector<const double*>& in, const std::vector<double*>& out) -> int {
+    if (!R.single) {
+      for (int r = 0; r < n; ++r) {
+        mr_ctx* c = cs[r];
+        sdev(c);
+        if (fast) {
+          int rc = eval_fast_dev(c, in[r], out[r], sst(c, st));
+          if (rc) return rc;
+        } else {
+          MR_CUDA_TRY(c, cudaMemsetAsync(out[r], 0, c->dof * sizeof(double), sst(c, st)));
+        }
+      }
+      return MR_OK;
+    }
+    for (int r = 0; r < n; ++r)
+      if (fast) {
+        sdev(cs[r]);
+        int rc = eval_fast_dev(cs[r], in[r], scrF(r), sst(cs[r], st));
+        if (rc) return rc;
+      }
+    std::vector<double*> oi(n);
+    for (int r = 0; r < n; ++r) oi[r] = scrI(r);
+    if (imp) {
+      int rc = eval_implicit(cs, n, in.data(), oi.data(), st);
+      if (rc) return rc;
+    }
+    if (slow) {
+      int rc = eval_slow(cs, n, in.data(), out.data(), st);
+      if (rc) return rc;
+    }
+    for (int r = 0; r < n; ++r) {
+      mr_ctx* c = cs[r];
+      sdev(c);
+      MR_CUDA_TRY(c, launch_sum_rhs(c->dof, fast ? scrF(r) : nullptr, imp ? scrI(r) : nullptr,
+                                    slow ? out[r] : nullptr, out[r], sst(c, st)));
+      c->launches++;
+    }
+    return MR_OK;
+  };
+  // slow_rhs (partitioned_system.hpp:54-60): implicit then explicit
+  auto eval_coarse = [&](const std::vector<const double*>& in, const std::vector<double*>& out) -> int {
+    std::vector<double*> oi(n);
+    for (int r = 0; r < n; ++r) oi[r] = scrI(r);
+    if (imp) {
+      int rc = eval_implicit(cs, n, in.data(), oi.data(), st);
+      if (rc) return rc;
+    }
+    if (slow) {
+      int rc = eval_slow(cs, n, in.data(), out.data(), st);
+      if (rc) return rc;
+    }
+    for (int r = 0; r < n; ++r) {
+      mr_ctx* c = cs[r];
+      sdev(c);
+      MR_CUDA_TRY(c, launch_sum_rhs(c->dof, nullptr, imp ? scrI(r) : nullptr,
+                                    slow ? out[r] : nullptr, out[r], sst(c, st)));
+      c->launches++;
+    }
+    return MR_OK;
+  };
+  // evaluations of one sweep (and of the coarse nodes it reaches before node k)
+  int coarse_hits = 0;
+  for (int q = 1; q < nf; ++q) coarse_hits += !R.single && R.coarse_index_of_fine[q] >= 0;
+  for (int r = 0; r < n; ++r) {
+    sdev(cs[r]);
+    MR_CUDA_TRY(cs[r], cudaMemcpyAsync(backup(r), cs[r]->y_state, cs[r]->dof * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, sst(cs[r], st)));
+  }
+  const long n_steps = (long)std::ceil((tf - t0) / H - 1e-12);
+  double t = t0;
+  for (long ns = 0; ns < n_steps; ++ns) {
+    const double step = (ns == n_steps - 1) ? (tf - t) : H;
+    for (int r = 0; r < n; ++r) {
+      sdev(cs[r]);
+      MR_CUDA_TRY(cs[r], cudaMemsetAsync(cs[r]->d_fail, 0xFF, sizeof(unsigned long long),
+                                         sst(cs[r], st)));
+    }
+    // initial caches: the step's state at every node
+    for (int r = 0; r < n; ++r) {
+      yc[r] = cs[r]->y_state;
+      oc[r] = fcur[r][0];
+    }
+    int rc = eval_fine(yc, oc);
+    if (rc) return rc;
+    if (X > 0) {
+      for (int r = 0; r < n; ++r) oc[r] = scur[r][0];
+      rc = eval_coarse(yc, oc);
+      if (rc) return rc;
+    }
+    for (int r = 0; r < n; ++r) {
+      mr_ctx* c = cs[r];
+      sdev(c);
+      const size_t bytes = c->dof * sizeof(double);
+      for (int q = 1; q < nf; ++q)
+        MR_CUDA_TRY(c, cudaMemcpyAsync(fcur[r][q], fcur[r][0], bytes, cudaMemcpyDeviceToDevice, sst(c, st)));
+      for (int p = 1; p < X; ++p)
+        MR_CUDA_TRY(c, cudaMemcpyAsync(scur[r][p], scur[r][0], bytes, cudaMemcpyDeviceToDevice, sst(c, st)));
+    }
+    for (int sw = 0; sw < R.sweeps; ++sw) {
+      // the k-th iterate's caches (read) and fresh slots for the (k+1)-th
+      std::vector<std::vector<double*>> fold = fcur, sold = scur;
+      for (int q = 0; q < nf - 1; ++q) {
+        const double hq = (R.fine_nodes[q + 1] - R.fine_nodes[q]) * step;
+        const int p = R.single ? 0 : R.coarse_of_fine[q];
+        const int key_stage = sw * 4096 + q + 1;
+        for (int r = 0; r < n; ++r) {
+          mr_ctx* c = cs[r];
+          sdev(c);
+          const double* f[2 * MR_MAXREF];
+          double cf[2 * MR_MAXREF];
+          int nt = 0;
+          const int Yn = R.single ? nf : R.Y;
+          const int off = R.single ? 0 : R.application_offset[q];
+          for (int j = 0; j < Yn; ++j) {
+            const double w = R.fine_row[(size_t)q * Yn + j];
+            if (w != 0.0) { f[nt] = fold[r][off + j]; cf[nt++] = step * w; }
+          }
+          for (int j = 0; j < X; ++j) {
+            const double w = R.coarse_row[(size_t)q * X + j];
+            if (w != 0.0) { f[nt] = sold[r][j]; cf[nt++] = step * w; }
+          }
+          f[nt] = fcur[r][q]; cf[nt++] = hq;
+          f[nt] = fold[r][q]; cf[nt++] = -hq;
+          if (X > 0) {
+            f[nt] = scur[r][p]; cf[nt++] = hq;
+            f[nt] = sold[r][p]; cf[nt++] = -hq;
+          }
+          const double* src = q == 0 ? c->y_state : node(r, q);
+          double* dst = node(r, q + 1);
+          // the terms in order, in launches of at most MR_MAXREF (sequential adds)
+          for (int a = 0; a < nt; a += MR_MAXREF) {
+            const int na = std::min(MR_MAXREF, nt - a);
+            MR_CUDA_TRY(c, launch_update(a == 0 ? src : dst, dst, na, f + a, cf + a, c->dof,
+                                         key_stage, c->d_fail, sst(c, st)));
+            c->launches++;
+          }
+          yc[r] = dst;
+          oc[r] = fspare[r][q + 1];
+        }
+        rc = eval_fine(yc, oc);
+        if (rc) return rc;
+        for (int r = 0; r < n; ++r) std::swap(fcur[r][q + 1], fspare[r][q + 1]);
+        const int cp = R.single ? -1 : R.coarse_index_of_fine[q + 1];
+        if (cp >= 0) {
+          for (int r = 0; r < n; ++r) oc[r] = sspare[r][cp];
+          rc = eval_coarse(yc, oc);
+          if (rc) return rc;
+          for (int r = 0; r < n; ++r) std::swap(scur[r][cp], sspare[r][cp]);
+        }
+      }
+    }
+    // failure key of this step (min over slabs / ranks)
+    for (int r = 0; r < n; ++r) {
+      mr_ctx* c = cs[r];
+      sdev(c);
+      if (c->comm)
+        MR_NCCL_TRY(c, AllReduce(c->d_fail, c->d_fail, 1, ncclUint64, ncclMin, c->comm, sst(c, st)));
+      MR_CUDA_TRY(c, cudaMemcpyAsync(c->h_fail, c->d_fail, sizeof(unsigned long long),
+                                     cudaMemcpyDeviceToHost, sst(c, st)));
+    }
+    unsigned long long key = MR_NO_FAIL;
+    for (int r = 0; r < n; ++r) {
+      sdev(cs[r]);
+      MR_CUDA_TRY(cs[r], cudaStreamSynchronize(sst(cs[r], st)));
+      key = std::min(key, *cs[r]->h_fail);
+    }
+    const uint64_t per_fast = (uint64_t)(nf - 1), per_slow = (uint64_t)coarse_hits;
+    if (key != MR_NO_FAIL) {
+      const int m = (int)(key >> 40), sw = m / 4096, k = m % 4096;  // node k failed in sweep sw
+      int hits = 0;
+      for (int q = 1; q < k; ++q) hits += !R.single && R.coarse_index_of_fine[q] >= 0;
+      if (cnt_fast && (fast || R.single)) *cnt_fast += (uint64_t)nf + (uint64_t)sw * per_fast + (uint64_t)(k - 1);
+      if (cnt_slow && !R.single) *cnt_slow += (uint64_t)X + (uint64_t)sw * per_slow + (uint64_t)hits;
+      if (fail_stage) *fail_stage = k;
+      for (int r = 0; r < n; ++r) {
+        sdev(cs[r]);
+        MR_CUDA_TRY(cs[r], cudaMemcpyAsync(cs[r]->y_state, backup(r), cs[r]->dof * sizeof(double),
+                                           cudaMemcpyDeviceToDevice, sst(cs[r], st)));
+        MR_CUDA_TRY(cs[r], cudaStreamSynchronize(sst(cs[r], st)));
+      }
+      return set_err(c0, MR_INTEGRATION,
+                     std::string(R.single ? "sdc_step" : "mrsdc_sweep") +
+                         ": non-finite update at node " + std::to_string(k));
+    }
+    if (cnt_fast && (fast || R.single)) *cnt_fast += (uint64_t)nf + (uint64_t)R.sweeps * per_fast;
+    if (cnt_slow && !R.single) *cnt_slow += (uint64_t)X + (uint64_t)R.sweeps * per_slow;
+    // the last fine node is the step's result
+    for (int r = 0; r < n; ++r) {
+      mr_ctx* c = cs[r];
+      sdev(c);
+      if (R.sweeps > 0) {
+        MR_CUDA_TRY(c, cudaMemcpyAsync(c->y_work, node(r, nf - 1), c->dof * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, sst(c, st)));
+        std::swap(c->y_state, c->y_work);
+      }
+    }
+    t = (ns == n_steps - 1) ? tf : t0 + (double)(ns + 1) * H;
+  }
+  return MR_OK;
+}
+
+// ---- SDC node sets (restated from proj/src/sdc.cpp:14-150 with the same
+// arithmetic order, so the tables are bitwise the reference's) ----
+namespace {
+// integral over [a, b] of the Lagrange basis polynomial j of `x` (sdc.cpp:14-41):
+// the monomial coefficients of prod_{m != j} (t - x_m), integrated term by
+// term, divided by prod_{m != j} (x_j - x_m)
+double lagrange_basis_integral(const std::vector<double>& x, int j, double a, double b)
+{
+  std::vector<double> c{1.0};
+  double den = 1.0;
+  for (int m = 0; m < (int)x.size(); ++m) {
+    if (m == j) continue;
+    std::vector<double> nc(c.size() + 1, 0.0);
+    for (size_t k = 0; k < c.size(); ++k) {
+      nc[k + 1] += c[k];
+      nc[k] -= x[m] * c[k];
+    }
+    c.swap(nc);
+    den *= x[j] - x[m];
+  }
+  double sum = 0.0, bk = b, ak = a;
+  for (size_t k = 0; k < c.size(); ++k) {
+    sum += c[k] * (bk - ak) / (double)(k + 1);
+    bk *= b;
+    ak *= a;
+  }
+  return sum / den;
+}
+
+// Gauss-Lobatto nodes on [0, 1] (n = 3 or 5) and S[q][j] = integral of basis
+// j over [x_q, x_{q+1}] (sdc.cpp:60-80)
+bool lobatto_rule(int n, std::vector<double>& x, std::vector<double>& S)
+{
+  if (n == 3) {
+    x = {0.0, 0.5, 1.0};
+  } else if (n == 5) {
+    const double r = std::sqrt(3.0 / 7.0);
+    x = {0.0, 0.5 * (1.0 - r), 0.5, 0.5 * (1.0 + r), 1.0};
+  } else {
+    return false;
+  }
+  S.assign((size_t)(n - 1) * n, 0.0);
+  for (int q = 0; q + 1 < n; ++q)
+    for (int j = 0; j < n; ++j) S[(size_t)q * n + j] = lagrange_basis_integral(x, j, x[q], x[q + 1]);
+  return true;
+}
+
+constexpr double kSdcNodeTol = 1.0e-12;  // sdc.cpp:10
+
+// build_scheme(X, Y, Z, n_sweeps) (sdc.cpp:82-153): X coarse Lobatto nodes,
+// each coarse interval split into Z applications of the Y-node rule, the
+// shared junction nodes merged
+int mrsdc_tables(int X, int Y, int Z, mr_ctx::SdcScheme& M)
+{
+  if ((X != 3 && X != 5) || (Y != 3 && Y != 5) || Z < 1) return 1;
+  std::vector<double> xc, Sc, xf, Sf;
+  lobatto_rule(X, xc, Sc);
+  lobatto_rule(Y, xf, Sf);
+  std::vector<double> start, width;
+  for (int p = 0; p + 1 < X; ++p) {
+    const double w = (xc[p + 1] - xc[p]) / Z;
+    for (int z = 0; z < Z; ++z) {
+      start.push_back(xc[p] + z * w);
+      width.push_back(w);
+    }
+  }
+  M.fine_nodes.assign(1, 0.0);
+  std::vector<int> first;
+  for (size_t a = 0; a < start.size(); ++a) {
+    first.push_back((int)M.fine_nodes.size() - 1);
+    for (int j = 1; j < Y; ++j) M.fine_nodes.push_back(start[a] + xf[j] * width[a]);
+  }
+  const int nf = (int)M.fine_nodes.size();
+  if (nf != X + (X - 1) * (Z - 1) + (X - 1) * (Y - 2) * Z) return 1;
+  M.X = X;
+  M.Y = Y;
+  M.n_fine = nf;
+  M.coarse_nodes = xc;
+  M.fine_row.assign((size_t)(nf - 1) * Y, 0.0);
+  M.application_offset.assign(nf - 1, 0);
+  M.coarse_row.assign((size_t)(nf - 1) * X, 0.0);
+  int app = 0;
+  for (int q = 0; q + 1 < nf; ++q) {
+    while (app + 1 < (int)start.size() && M.fine_nodes[q] >= start[app + 1] - kSdcNodeTol) ++app;
+    const int local = q - first[app];
+    for (int j = 0; j < Y; ++j) M.fine_row[(size_t)q * Y + j] = width[app] * Sf[(size_t)local * Y + j];
+    M.application_offset[q] = first[app];
+    for (int j = 0; j < X; ++j)
+      M.coarse_row[(size_t)q * X + j] =
+          lagrange_basis_integral(xc, j, M.fine_nodes[q], M.fine_nodes[q + 1]);
+  }
+  M.coarse_of_fine.assign(nf, 0);
+  M.coarse_index_of_fine.assign(nf, -1);
+  for (int q = 0; q < nf; ++q) {
+    int p = 0;
+    for (int j = 0; j < X; ++j)
+      if (xc[j] <= M.fine_nodes[q] + kSdcNodeTol) p = j;
+    M.coarse_of_fine[q] = p;
+    if (std::fabs(xc[p] - M.fine_nodes[q]) < kSdcNodeTol) M.coarse_index_of_fine[q] = p;
+  }
+  return 0;
+}
+}  // namespace
+
+int mr_lobatto_rule(int n, double* nodes, double* S)
+{
+  std::vector<double> x, s;
+  if (!nodes || !S || !lobatto_rule(n, x, s)) return MR_CONTRACT;
+  std::memcpy(nodes, x.data(), x.size() * sizeof(double));
+  std::memcpy(S, s.data(), s.size() * sizeof(double));
+  return MR_OK;
+}
+
+int mr_mrsdc_scheme(int X, int Y, int Z, int* n_fine, double* coarse_nodes, double* fine_nodes,
+                    int* coarse_of_fine, int* coarse_index_of_fine, double* fine_row,
+                    int* application_offset, double* coarse_row)
+{
+  mr_ctx::SdcScheme M;
+  if (!n_fine || mrsdc_tables(X, Y, Z, M)) return MR_CONTRACT;
+  const int nf = M.n_fine;
+  const bool want = coarse_nodes && fine_nodes && coarse_of_fine && coarse_index_of_fine &&
+                    fine_row && application_offset && coarse_row;
+  if (want && *n_fine < nf) return MR_CONTRACT;
+  *n_fine = nf;
+  if (!want) return MR_OK;  // size query
+  std::memcpy(coarse_nodes, M.coarse_nodes.data(), X * sizeof(double));
+  std::memcpy(fine_nodes, M.fine_nodes.data(), nf * sizeof(double));
+  std::memcpy(coarse_of_fine, M.coarse_of_fine.data(), nf * sizeof(int));
+  std::memcpy(coarse_index_of_fine, M.coarse_index_of_fine.data(), nf * sizeof(int));
+  std::memcpy(fine_row, M.fine_row.data(), M.fine_row.size() * sizeof(double));
+  std::memcpy(application_offset, M.application_offset.data(), (nf - 1) * sizeof(int));
+  std::memcpy(coarse_row, M.coarse_row.data(), M.coarse_row.size() * sizeof(double));
+  return MR_OK;
+}
+
+int mr_mrsdc_build(mr_ctx* c, int X, int Y, int Z, int n_sweeps)
+{
+  if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
+  MR_FORWARD(c, mr_mrsdc_build(sl_, X, Y, Z, n_sweeps));
+  mr_ctx::SdcScheme M;
+  if (n_sweeps < 1 || mrsdc_tables(X, Y, Z, M))
+    return set_err(c, MR_CONTRACT, "build_scheme: need X,Y in {3,5}, Z >= 1, sweeps >= 1");
+  M.n_sweeps = n_sweeps;
+  M.loaded = true;
+  c->mrsdc = M;
+  return MR_OK;
+}
+
+int mr_sdc_integrate(mr_ctx* c, int n_nodes, const double* nodes, const double* S, int n_sweeps,
+                     double t0, double tf, double H, uint64_t* n_evals, int* fail_stage)
+{
+  if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
+  if (!nodes || !S || n_nodes < 2 || n_nodes > MR_MAXREF - 2 || n_sweeps < 0)
+    return set_err(c, MR_CONTRACT, "sdc_integrate: 2 <= nodes <= 10, S[(n-1) x n], sweeps >= 0");
+  SdcRun R{};
+  R.single = true;
+  R.nf = n_nodes;
+  R.Y = n_nodes;
+  R.sweeps = n_sweeps;
+  R.fine_nodes = nodes;
+  R.fine_row = S;
+  if (!c->slabs.empty())
+    return domain_rc(c, sdc_integrate_dev(c->slabs.data(), (int)c->slabs.size(), R, t0, tf, H,
+                                          n_evals, nullptr, fail_stage));
+  return sdc_integrate_dev(&c, 1, R, t0, tf, H, n_evals, nullptr, fail_stage);
+}
+
+int mr_mrsdc_load(mr_ctx* c, int X, int Y, int n_fine, int n_sweeps, const double* coarse_nodes,
+                  const double* fine_nodes, const int* coarse_of_fine,
+                  const int* coarse_index_of_fine, const double* fine_row,
+                  const int* application_offset, const double* coarse_row)
+{
+  if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
+  MR_FORWARD(c, mr_mrsdc_load(sl_, X, Y, n_fine, n_sweeps, coarse_nodes, fine_nodes,
+                              coarse_of_fine, coarse_index_of_fine, fine_row, application_offset,
+                              coarse_row));
+  if (X < 2 || Y < 2 || n_fine < 2 || n_fine > 4095 || n_sweeps < 0 || Y + X + 4 > 2 * MR_MAXREF ||
+      !coarse_nodes || !fine_nodes || !coarse_of_fine || !coarse_index_of_fine || !fine_row ||
+      !application_offset || !coarse_row)
+    return set_err(c, MR_CONTRACT, "mr_mrsdc_load: bad scheme");
+  auto& M = c->mrsdc;
+  M.X = X;
+  M.Y = Y;
+  M.n_fine = n_fine;
+  M.n_sweeps = n_sweeps;
+  M.coarse_nodes.assign(coarse_nodes, coarse_nodes + X);
+  M.fine_nodes.assign(fine_nodes, fine_nodes + n_fine);
+  M.coarse_of_fine.assign(coarse_of_fine, coarse_of_fine + n_fine);
+  M.coarse_index_of_fine.assign(coarse_index_of_fine, coarse_index_of_fine + n_fine);
+  M.fine_row.assign(fine_row, fine_row + (size_t)(n_fine - 1) * Y);
+  M.application_offset.assign(application_offset, application_offset + (n_fine - 1));
+  M.coarse_row.assign(coarse_row, coarse_row + (size_t)(n_fine - 1) * X);
+  for (int q = 0; q < n_fine; ++q)
+    if (M.coarse_of_fine[q] < 0 || M.coarse_of_fine[q] >= X || M.coarse_index_of_fine[q] >= X)
+      return set_err(c, MR_CONTRACT, "mr_mrsdc_load: coarse index out of range");
+  for (int q = 0; q + 1 < n_fine; ++q)
+    if (M.application_offset[q] < 0 || M.application_offset[q] + Y > n_fine)
+      return set_err(c, MR_CONTRACT, "mr_mrsdc_load: application offset out of range");
+  M.loaded = true;
+  return MR_OK;
+}
+
+int mr_mrsdc_integrate(mr_ctx* c, double t0, double tf, double H, uint64_t* counters,
+                       int* fail_stage)
+{
+  if (!c) return MR_CONTRACT;
+  if (int g = pending_guard(c)) return g;
+  mr_ctx* m = c->slabs.empty() ? c : c->slabs[0];
+  if (!m->mrsdc.loaded) return set_err(c, MR_CONTRACT, "mrsdc_integrate: no scheme (mr_mrsdc_load)");
+  const auto& M = m->mrsdc;
+  SdcRun R{};
+  R.single = false;
+  R.X = M.X;
+  R.Y = M.Y;
+  R.nf = M.n_fine;
+  R.sweeps = M.n_sweeps;
+  R.coarse_nodes = M.coarse_nodes.data();
+  R.fine_nodes = M.fine_nodes.data();
+  R.fine_row = M.fine_row.data();
+  R.coarse_row = M.coarse_row.data();
+  R.coarse_of_fine = M.coarse_of_fine.data();
+  R.coarse_index_of_fine = M.coarse_index_of_fine.data();
+  R.application_offset = M.application_offset.data();
+  uint64_t* cf = counters ? counters + MR_CNT_FAST_EVALS : nullptr;
+  uint64_t* cx = counters ? counters + MR_CNT_EXPLICIT_EVALS : nullptr;
+  if (!c->slabs.empty())
+    return domain_rc(c, sdc_integrate_dev(c->slabs.data(), (int)c->slabs.size(), R, t0, tf, H, cf,
+                                          cx, fail_stage));
+  return sdc_integrate_dev(&c, 1, R, t0, tf, H, cf, cx, fail_stage);
 }
 
 // reference_solution (erk.cpp:59-75): erk_integrate of cash-karp5

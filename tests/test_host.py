@@ -192,3 +192,19 @@ def test_routed_harness_runs_cpu_studies_unchanged(tmp_path):
     assert rows[0].startswith("method,H,tolerance,error,rate") and len(rows) == n + 1
     for name, order, s in zip(methods, [3, 4, 3, 4], slopes):
         assert s > order - 0.5, (name, s)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_sdc_node_sets_bitwise_reference():
+    """lobatto_nodes / build_scheme restated in the library (host code, no GPU)
+    are bitwise the reference's own tables (proj/src/sdc.cpp:14-153)."""
+    for n in (3, 5):
+        a, b = P.lobatto_rule(n), O.ref_lobatto_nodes(n)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    for X, Y, Z in [(3, 3, 1), (3, 3, 8), (5, 3, 2), (3, 5, 4), (5, 5, 3)]:
+        a, b = P.mrsdc_scheme(X, Y, Z), O.ref_mrsdc_scheme(X, Y, Z)
+        assert a["n_fine"] == b["n_fine"] == X + (X - 1) * (Z - 1) + (X - 1) * (Y - 2) * Z
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
+    with pytest.raises(P.ContractError):
+        P.mrsdc_scheme(4, 3, 1)
