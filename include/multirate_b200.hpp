@@ -25,6 +25,7 @@
 
 #include "mri_b200.h"
 #include "multirate/mri.hpp"
+#include "multirate/sdc.hpp"
 
 namespace multirate::b200 {
 
@@ -254,6 +255,57 @@ inline StateVector ark_imex_integrate(Device& d, const ImplicitStageSolver& solv
   to_c(counters, c);
   int stage = -1;
   const int rc = mr_ark_imex_integrate(d.ctx(), t0, tf, H, c, &stage);
+  from_c(c, counters);
+  d.check(rc, stage);
+  StateVector out(y0.size());
+  d.check(mr_state_download(d.ctx(), out.data()));
+  return out;
+}
+
+// sdc_integrate (sdc.cpp:267-281) of f_fast + f_implicit + f_explicit on the
+// device plugins with the reference's node set: the harness's sdc-<sweeps>
+// family (harness.cpp:356-366), evaluations counted into *eval_counter
+inline StateVector sdc_integrate(Device& d, const QuadratureNodes& nodes, double t0, double tf,
+                                 double H, const StateVector& y0, int n_sweeps,
+                                 std::size_t* eval_counter = nullptr)
+{
+  if (y0.size() != d.dof()) throw ContractError("sdc_integrate: state size != grid dof");
+  const int n = nodes.n;
+  std::vector<double> S(static_cast<size_t>(n > 0 ? n - 1 : 0) * n);
+  for (int q = 0; q + 1 < n; ++q)
+    for (int j = 0; j < n; ++j) S[static_cast<size_t>(q) * n + j] = nodes.S[q][j];
+  d.check(mr_state_upload(d.ctx(), y0.data()));
+  uint64_t evals = 0;
+  int stage = -1;
+  const int rc = mr_sdc_integrate(d.ctx(), n, nodes.nodes.data(), S.data(), n_sweeps, t0, tf, H,
+                                  &evals, &stage);
+  if (eval_counter) *eval_counter += static_cast<std::size_t>(evals);
+  d.check(rc, stage);
+  StateVector out(y0.size());
+  d.check(mr_state_download(d.ctx(), out.data()));
+  return out;
+}
+
+// mrsdc_integrate (sdc.cpp:283-301) of a build_scheme(X, Y, Z, sweeps) scheme
+// on the device plugins: the harness's mrsdc-XYZ family (harness.cpp:368-372)
+inline StateVector mrsdc_integrate(Device& d, const MrsdcScheme& s, double t0, double tf, double H,
+                                   const StateVector& y0, EvalCounters& counters)
+{
+  if (y0.size() != d.dof()) throw ContractError("mrsdc_integrate: state size != grid dof");
+  const int nf = s.n_fine, X = s.X, Y = s.Y;
+  std::vector<double> frow(static_cast<size_t>(nf - 1) * Y), crow(static_cast<size_t>(nf - 1) * X);
+  for (int q = 0; q + 1 < nf; ++q) {
+    for (int j = 0; j < Y; ++j) frow[static_cast<size_t>(q) * Y + j] = s.fine_row[q][j];
+    for (int j = 0; j < X; ++j) crow[static_cast<size_t>(q) * X + j] = s.coarse_row[q][j];
+  }
+  d.check(mr_mrsdc_load(d.ctx(), X, Y, nf, s.n_sweeps, s.coarse.nodes.data(), s.fine_nodes.data(),
+                        s.coarse_of_fine.data(), s.coarse_index_of_fine.data(), frow.data(),
+                        s.application_offset.data(), crow.data()));
+  d.check(mr_state_upload(d.ctx(), y0.data()));
+  uint64_t c[8];
+  to_c(counters, c);
+  int stage = -1;
+  const int rc = mr_mrsdc_integrate(d.ctx(), t0, tf, H, c, &stage);
   from_c(c, counters);
   d.check(rc, stage);
   StateVector out(y0.size());

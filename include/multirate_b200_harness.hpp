@@ -7,12 +7,16 @@
 //   -Dmri_integrate=mri_integrate_routed
 //   -Dark_imex_integrate=ark_imex_integrate_routed
 //   -Derk_integrate=erk_integrate_routed
+//   -Dsdc_integrate=sdc_integrate_routed
+//   -Dmrsdc_integrate=mrsdc_integrate_routed
 //
-// so run_method's Mri, ArkImex and Erk cases call the three routing functions
+// so every case of run_method -- Mri, ArkImex, Erk, Sdc, Mrsdc -- calls one of
+// the five routing functions
 // declared below (their definitions are compiled once, WITHOUT those macros,
 // in a translation unit that defines MULTIRATE_B200_HARNESS_IMPL before
 // including this header).  A routed problem (b200::route) goes to the facade
-// -- mri_integrate / ark_imex_integrate / erk_integrate on the device-resident
+// -- mri_integrate / ark_imex_integrate / erk_integrate / sdc_integrate /
+// mrsdc_integrate on the device-resident
 // state, the counters filled exactly like the reference's -- and every other
 // problem to the reference's own integrators, so CPU studies are unchanged.
 // run_method's divergence handling (IntegrationError -> RunOutcome::diverged,
@@ -31,6 +35,7 @@
 #include "multirate/erk.hpp"
 #include "multirate/harness.hpp"
 #include "multirate/mri.hpp"
+#include "multirate/sdc.hpp"
 
 namespace multirate {
 
@@ -42,6 +47,12 @@ StateVector ark_imex_integrate_routed(const ArkPair& pair, const PartitionedSyst
                                       double H, const StateVector& y0, EvalCounters& counters);
 StateVector erk_integrate_routed(const ButcherTable& table, const RhsFn& f, double t0, double tf,
                                  double h, const StateVector& y0, std::size_t* eval_counter);
+StateVector sdc_integrate_routed(const QuadratureNodes& nodes, const RhsFn& f_total, double t0,
+                                 double tf, double H, const StateVector& y0, int n_sweeps,
+                                 std::size_t* eval_counter);
+StateVector mrsdc_integrate_routed(const MrsdcScheme& scheme, const PartitionedSystem& system,
+                                   double t0, double tf, double H, const StateVector& y0,
+                                   EvalCounters& counters);
 
 }  // namespace multirate
 
@@ -134,6 +145,25 @@ StateVector erk_integrate_routed(const ButcherTable& table, const RhsFn& f, doub
   if (b200::Device* d = b200::routed_device(y0))
     return b200::erk_integrate(*d, table, t0, tf, h, y0, eval_counter);
   return erk_integrate(table, f, t0, tf, h, y0, eval_counter);
+}
+
+StateVector sdc_integrate_routed(const QuadratureNodes& nodes, const RhsFn& f_total, double t0,
+                                 double tf, double H, const StateVector& y0, int n_sweeps,
+                                 std::size_t* eval_counter)
+{
+  // run_method's Sdc case integrates problem.system.sum_rhs (harness.cpp:356-366)
+  if (b200::Device* d = b200::routed_device(y0))
+    return b200::sdc_integrate(*d, nodes, t0, tf, H, y0, n_sweeps, eval_counter);
+  return sdc_integrate(nodes, f_total, t0, tf, H, y0, n_sweeps, eval_counter);
+}
+
+StateVector mrsdc_integrate_routed(const MrsdcScheme& scheme, const PartitionedSystem& system,
+                                   double t0, double tf, double H, const StateVector& y0,
+                                   EvalCounters& counters)
+{
+  if (b200::Device* d = b200::routed_device(y0))
+    return b200::mrsdc_integrate(*d, scheme, t0, tf, H, y0, counters);
+  return mrsdc_integrate(scheme, system, t0, tf, H, y0, counters);
 }
 
 }  // namespace multirate

@@ -1,9 +1,9 @@
 """The reference's study harness on a device problem.
 
 oracle/_ref/libharness_test.so links proj/src/harness.cpp compiled UNMODIFIED
-with the routing prefix of include/multirate_b200_harness.hpp: run_method's
-Mri, ArkImex and Erk cases (harness.cpp:346-394) go to the facade for a
-routed device problem.  The same study runs on the CPU physics (the
+with the routing prefix of include/multirate_b200_harness.hpp: every case of
+run_method -- Mri, ArkImex, Erk, Sdc, Mrsdc (harness.cpp:346-394) -- goes to
+the facade for a routed device problem.  The same study runs on the CPU physics (the
 reference's own integrators) and routed to the GPU, through the reference's
 run_method / measure_error / fitted_slope / RunReport::write_csv; the two
 CSVs (harness.cpp:645-663) must agree row by row: same methods, H, steps and
@@ -105,3 +105,16 @@ def test_diverging_run_is_recorded_not_thrown(tmp_path):
     cpu, dev, _ = _run(tmp_path, "C1", 8, ["erk-kutta3"], [2e-15], 4e-15, 2e-18)
     _compare(cpu, dev)
     assert dev[0]["diverged"] == "1" and cpu[0]["diverged"] == "1"
+
+
+def test_sdc_study_rows_cpu_vs_routed_device(tmp_path):
+    """run_method's Sdc and Mrsdc cases (harness.cpp:356-372) routed to the
+    device SDC integrators: sdc-2 (lobatto 3) at fast-scale steps and
+    mrsdc-335 at slow-scale steps on the C1 chemistry + transport, cash-karp5
+    reference -- the routed rows equal the CPU rows."""
+    cpu, dev, _ = _run(tmp_path, "C1", 8, ["sdc-2"], [4e-17, 2e-17], 1.6e-16, 2e-19)
+    _compare(cpu, dev)
+    cpu, dev, js = _run(tmp_path, "C1", 8, ["mrsdc-335"], [1.2e-16, 6e-17, 3e-17], 4.8e-16, 3e-19)
+    _compare(cpu, dev)
+    assert all(r["diverged"] == "0" for r in dev)
+    print({k: round(v, 2) for k, v in js["fitted_slopes"].items()})
