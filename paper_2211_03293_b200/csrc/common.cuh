@@ -89,9 +89,6 @@ struct ChemParams {
   // in uint4 words relative to ent_base; entries are byte offsets of q rows
   // (chunk-local), lists padded to 4 with the offset of an all-zero row
   ushort4 lst[MR_CHEM_MAXS][MR_CHEM_MAXCHUNK];
-  // slot (w + NW*t) -> component owned by that thread; >= ncomp = idle.
-  // Greedy-balanced on the species' production-list lengths.
-  unsigned char perm[MR_CHEM_MAXS];
   unsigned long long* prof;  // phase-cycle accumulators (MR_PHASE_PROF builds only)
 };
 

@@ -41,11 +41,6 @@ namespace mrchem {
 #endif
 constexpr int kRxUnroll = MR_RX_UNROLL;  // reaction-loop unroll (ILP)
 
-#ifndef MR_CHEM_PERM
-#define MR_KK(slot) (slot)
-#else
-#define MR_KK(slot) (P.perm[slot])
-#endif
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -70,28 +65,6 @@ __device__ __forceinline__ double mr_exp(double x)
 #pragma unroll
   for (int i = 1; i < 14; ++i) p = fma(p, r, kExpC[i]);
   return p * __hiloint2double((n + 1023) << 20, 0);
-}
-
-// exp(x) and exp(-x) together: one range reduction, two independent Horner
-// chains (e^-r = p(-r)), the reciprocal scale from the exponent bits.  Replaces
-// the 1/E division of the species rows (MUFU.RCP64H + Newton + slow-path
-// branch) by 14 independent DFMAs (MR_EXP_PAIR; measured 2% slower, off).
-__device__ __forceinline__ void mr_exp_pair(double x, double& e, double& ei)
-{
-  const double t = fma(x, kExpC[14], 6755399441055744.0);
-  const double nd = t - 6755399441055744.0;
-  const int n = min(max(__double2loint(t), -1022), 1022);
-  double r = fma(nd, kExpC[15], x);
-  r = fma(nd, -5.49792301870837115524e-14, r);
-  const double rm = -r;
-  double p = kExpC[0], pm = kExpC[0];
-#pragma unroll
-  for (int i = 1; i < 14; ++i) {
-    p = fma(p, r, kExpC[i]);
-    pm = fma(pm, rm, kExpC[i]);
-  }
-  e = p * __hiloint2double((n + 1023) << 20, 0);
-  ei = pm * __hiloint2double((1023 - n) << 20, 0);
 }
 
 // shared memory (bytes are what the offset tables index)
@@ -256,16 +229,8 @@ __device__ __forceinline__ void chem_block_eval(const ChemParams& P, const Smem&
       if (k < S) {
         const double2 c2h0 = m.spc[k * 5 + 1], ahb = m.spc[k * 5 + 2], s0rw = m.spc[k * 5 + 3];
         const double g = c2h0.y * invT + ahb.x * (1.0 - lnT) - ahb.y * T - s0rw.x;
-#ifndef MR_EXP_PAIR
-#define MR_EXP_PAIR 0
-#endif
-#if MR_EXP_PAIR
-        double E, Ei;
-        mr_exp_pair(g, E, Ei);
-#else
         const double E = mr_exp(g);
-        const double Ei = 1.0 / E;
-#endif
+        const double Ei = 1.0 / E;  // (exp(-g) by a second Horner chain: 2% slower, DESIGN (s))
         const double Ck = s0rw.y * v[t];
         *reinterpret_cast<double2*>(m.CE + k * 512 + lane16) = make_double2(Ck, Ei * iRTP);
         *reinterpret_cast<double*>(m.D + k * 256 + lane8) = (E * Ck) * RTP;
@@ -369,9 +334,11 @@ __global__ void __launch_bounds__(NW * 32, chem_min_blocks(NW, NDEG))
   const long long ph_begin = ph_last;
 #endif
   const Smem m = stage(reinterpret_cast<char*>(smem_raw), P, NW, c, w);
-  int kk[SPL];  // components owned by this thread (load-balanced permutation)
+  // components owned by this thread: slots w + NW t in order (a production-
+  // list-balanced assignment measured neutral, DESIGN experiment (y))
+  int kk[SPL];
 #pragma unroll
-  for (int t = 0; t < SPL; ++t) kk[t] = MR_KK(w + NW * t);
+  for (int t = 0; t < SPL; ++t) kk[t] = w + NW * t;
 
   double y[SPL];
 #pragma unroll
@@ -543,9 +510,11 @@ __global__ void __launch_bounds__(NW * 32) chem_rhs_kernel(const double* __restr
   const size_t cell = (size_t)blockIdx.x * 32 + c;
   const bool active = cell < nc;
   const Smem m = stage(reinterpret_cast<char*>(smem_raw), P, NW, c, w);
-  int kk[SPL];  // components owned by this thread (load-balanced permutation)
+  // components owned by this thread: slots w + NW t in order (a production-
+  // list-balanced assignment measured neutral, DESIGN experiment (y))
+  int kk[SPL];
 #pragma unroll
-  for (int t = 0; t < SPL; ++t) kk[t] = MR_KK(w + NW * t);
+  for (int t = 0; t < SPL; ++t) kk[t] = w + NW * t;
   double v[SPL], f[SPL];
 #pragma unroll
   for (int t = 0; t < SPL; ++t) {

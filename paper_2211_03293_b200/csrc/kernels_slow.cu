@@ -458,32 +458,24 @@ __global__ void __launch_bounds__(kV2Threads, (kV2Threads <= 256 ? 2 : 1)) stenc
 #endif
 constexpr int kV3TJ = MR_V3_TJ, kV3PF = MR_V3_PF;  // block-barrier version measured: PF 2/3/4/6 -> 45/46/51/40% of HBM at 256^3
 constexpr int kV3Threads = 16 * kV3TJ;      // 2 x 2 points per thread (compute threads)
-#ifndef MR_V3_PRODUCER
-#define MR_V3_PRODUCER 0
-#endif
-// + one producer warp that fills the ring (MR_V3_PRODUCER, needs MR_V3_MBAR)
-constexpr int kV3Block = kV3Threads + (MR_V3_PRODUCER ? 32 : 0);
-#ifndef MR_V3_MBAR
-#define MR_V3_MBAR 1
-#endif
-#ifndef MR_V3_LATE_ISSUE
-#define MR_V3_LATE_ISSUE 1
-#endif
+// (a dedicated producer warp filling the ring: 288 threads, the compute
+// threads spill -- DESIGN.md section 4)
+constexpr int kV3Block = kV3Threads;
 constexpr int kV3MaxPlanes = 512;  // planes per block (iper) staged profile terms
 template <int M>
 constexpr size_t v3_smem_bytes()
 {
-  // ring [R][RJ][RK] + (MR_V3_MBAR) full[R] and empty[R] mbarriers
+  // ring [R][RJ][RK] + full[R] and empty[R] mbarriers
   return (size_t)(M + kV3PF + 1) * (kV3TJ + 2 * M) * (kV2TK + 2 * M) * sizeof(double) +
          2 * kV3MaxPlanes * sizeof(double) +  // per-plane velocity-profile terms
-         (MR_V3_MBAR ? 2 * (M + kV3PF + 1) * sizeof(unsigned long long) : 0);
+         2 * (M + kV3PF + 1) * sizeof(unsigned long long);
 }
 
 // K2 v3 (order 8): as v2 with a 2 x 2 register block per thread (rows jl,
 // jl+1) -- the axis-1 rows jl - m and jl + 1 + m each serve two outputs per
 // column pair, cutting the shared wavefronts per point by ~30% -- one
 // 256-thread block per SM (240 registers) and a 4-plane prefetch.  The plane
-// ring is synchronised by per-slot full/empty mbarriers (MR_V3_MBAR): no block
+// ring is synchronised by per-slot full/empty mbarriers: no block
 // barrier in the march, so warps drift up to two planes apart.
 template <int M, int VK>
 __global__ void __launch_bounds__(kV3Block, kV3Threads <= 128 ? 2 : 1) stencil_v3_kernel(const StencilArgs a, int iper)
@@ -530,16 +522,12 @@ __global__ void __launch_bounds__(kV3Block, kV3Threads <= 128 ? 2 : 1) stencil_v
   }
   // plane-dependent profile terms of u_1 and u_2 for this block's planes
   // (after the ring and its mbarriers)
-  double* sprof = reinterpret_cast<double*>(ring + (size_t)R * RJ * RK + (MR_V3_MBAR ? 2 * R : 0));
+  double* sprof = reinterpret_cast<double*>(ring + (size_t)R * RJ * RK + 2 * R);
   if constexpr (VK == 1)
     for (int q = tid; q < ie - ib; q += kThreads) {
       sprof[q] = a.prof[(1 * 2 + 0) * a.nmax + a.i0 + ib + q];
       sprof[kV3MaxPlanes + q] = a.prof[(2 * 2 + 0) * a.nmax + a.i0 + ib + q];
     }
-#if !MR_V3_MBAR
-  __syncthreads();
-#endif
-#if MR_V3_MBAR
   // full[s]: the kThreads cp.async arrivals of the plane in slot s; empty[s]:
   // one arrival per warp when it has finished reading the plane in slot s.
   // Warps run up to one plane apart instead of meeting at a block barrier.
@@ -547,52 +535,15 @@ __global__ void __launch_bounds__(kV3Block, kV3Threads <= 128 ? 2 : 1) stencil_v
   unsigned long long* empty = full + R;
   if (tid == 0) {
     for (int q = 0; q < R; ++q) {
-      mbar_init(full + q, MR_V3_PRODUCER ? 32 : kThreads);
+      mbar_init(full + q, kThreads);
       mbar_init(empty + q, kThreads / 32);
     }
   }
   __syncthreads();
-#endif
-#if MR_V3_PRODUCER
-  static_assert(MR_V3_MBAR, "the producer warp needs the mbarrier ring");
-  if (ty == kV3TJ / 2) {  // producer warp: planes ib - ... ie + M - 1 into the ring
-    constexpr int NP = (RJ * CPR + 31) / 32;
-    int ps[NP], pd[NP];
-#pragma unroll
-    for (int u = 0; u < NP; ++u) {
-      const int c = tx + 32 * u;
-      pd[u] = -1;
-      ps[u] = 0;
-      if (c < RJ * CPR) {
-        const int r = c / CPR, cc = c - r * CPR;
-        ps[u] = ((j0 - M + r + n1) % n1) * n2 + (k0 - M + CW * cc + n2) % n2;
-        pd[u] = r * RK + CW * cc;
-      }
-    }
-    const int nfill = ie + M - ib;
-    for (int rel = 0; rel < nfill; ++rel) {
-      const int sl = rel % R;
-      if (rel >= R) mbar_wait(empty + sl, (unsigned)((rel - R) / R) & 1u);
-      const double* src = plane_ptr(ib + rel);
-      double* dst = ring + (size_t)sl * RJ * RK;
-#pragma unroll
-      for (int u = 0; u < NP; ++u) {
-        if (pd[u] < 0) continue;
-        if constexpr (CW == 2) cp_async16(dst + pd[u], src + ps[u]);
-        else cp_async8(dst + pd[u], src + ps[u]);
-      }
-      mbar_cp_async_arrive(full + sl);
-    }
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    return;
-  }
-#endif
   auto issue_to = [&](int ip, double* dst) {
-    if (!MR_V3_PRODUCER && ip < ie + M) {
-#if MR_V3_MBAR
+    if (ip < ie + M) {
       const int rel = ip - ib, sl = rel % R;
       if (rel >= R) mbar_wait(empty + sl, (unsigned)((rel - R) / R) & 1u);  // previous occupant read
-#endif
       const char* src = reinterpret_cast<const char*>(plane_ptr(ip));
 #pragma unroll
       for (int u = 0; u < NCH; ++u) {
@@ -600,23 +551,14 @@ __global__ void __launch_bounds__(kV3Block, kV3Threads <= 128 ? 2 : 1) stencil_v
         if constexpr (CW == 2) cp_async16(dst + coff_dst[u], src + coff_src[u]);
         else cp_async8(dst + coff_dst[u], src + coff_src[u]);
       }
-#if MR_V3_MBAR
       mbar_cp_async_arrive(full + sl);
-#endif
     }
-#if !MR_V3_MBAR
-    cp_async_commit();
-#endif
   };
   auto issue = [&](int ip) { issue_to(ip, slot(ip)); };
   // this thread may read plane ip from the ring (its copies landed, all threads')
   auto ready = [&](int ip) {
-#if MR_V3_MBAR
     const int rel = ip - ib;
     mbar_wait(full + rel % R, (unsigned)(rel / R) & 1u);
-#else
-    (void)ip;
-#endif
   };
   auto pair = [&](const double* t, int r, int c, double& v0, double& v1) {
     if constexpr (M % 2 == 0) {
@@ -643,17 +585,12 @@ __global__ void __launch_bounds__(kV3Block, kV3Threads <= 128 ? 2 : 1) stencil_v
     cadv0[p] = (VK == 0 ? a.u[0]
                         : P[(0 * 2 + 0) * nm + jA + (p >> 1)] + P[(0 * 2 + 1) * nm + kA + (p & 1)]) *
                a.inv_dx[0];
-#ifndef MR_V3_HOIST
-#define MR_V3_HOIST 1  // measured: 56.5 -> 58.4% of HBM at 256^3
-#endif
-#if MR_V3_HOIST
   double pk1[2], pj2[2];  // per-thread profile terms of u_1 (k) and u_2 (j)
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     pk1[e] = VK == 0 ? 0.0 : P[(1 * 2 + 1) * nm + kA + e];
     pj2[e] = VK == 0 ? 0.0 : P[(2 * 2 + 1) * nm + jA + e];
   }
-#endif
   // output rows jA, jA + 1 of plane i: running pointer
   double* orow = a.out + (size_t)comp * ncell + (size_t)ib * plane + (size_t)jA * n2 + kA;
 
@@ -668,13 +605,8 @@ __global__ void __launch_bounds__(kV3Block, kV3Threads <= 128 ? 2 : 1) stencil_v
       qv[2 * e][q] = __ldg(src);
       qv[2 * e + 1][q] = __ldg(src + 1);
     }
-#if MR_V3_MBAR
 #pragma unroll
   for (int q = M; q < 2 * M; ++q) ready(ib - M + q);
-#else
-  cp_async_wait<PF>();
-  __syncthreads();
-#endif
 #pragma unroll
   for (int q = M; q < 2 * M; ++q)
 #pragma unroll
@@ -687,40 +619,20 @@ __global__ void __launch_bounds__(kV3Block, kV3Threads <= 128 ? 2 : 1) stencil_v
       const int t = t0 + ph;
       if (t >= nplanes) break;
       const int i = ib + t;
-#if !MR_V3_MBAR
-      cp_async_wait<PF - 1>();
-      __syncthreads();
-#endif
       // ring slots: compile-time when the ring and the register queue have the
       // same period (R == Q, t0 a multiple of Q)
-#ifndef MR_V3_CSLOT
-#define MR_V3_CSLOT 1
-#endif
-      constexpr bool kCs = MR_V3_CSLOT && R == Q;
+      constexpr bool kCs = R == Q;
       double* const s_iss = kCs ? ring + (size_t)((ph + M + PF) % R) * RJ * RK : slot(i + M + PF);
       const double* const tq = kCs ? ring + (size_t)((ph + M) % R) * RJ * RK : slot(i + M);
       const double* const tc = kCs ? ring + (size_t)(ph % R) * RJ * RK : slot(i);
-#if !MR_V3_MBAR || !MR_V3_LATE_ISSUE
-      issue_to(i + M + PF, s_iss);
-#endif
       ready(i + M);
 #pragma unroll
       for (int e = 0; e < 2; ++e) pair(tq, jl + e, kl, qv[2 * e][(ph + 2 * M) % Q], qv[2 * e + 1][(ph + 2 * M) % Q]);
-#if !MR_V3_HOIST
-      const int ig = a.i0 + i;
-#endif
       double cadv1[2], cadv2[2];  // u_1 depends on (i, k), u_2 on (i, j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-#if MR_V3_HOIST
         cadv1[e] = (VK == 0 ? a.u[1] : sprof[t] + pk1[e]) * a.inv_dx[1];
         cadv2[e] = (VK == 0 ? a.u[2] : sprof[kV3MaxPlanes + t] + pj2[e]) * a.inv_dx[2];
-#else
-        cadv1[e] = (VK == 0 ? a.u[1] : P[(1 * 2 + 0) * nm + ig] + P[(1 * 2 + 1) * nm + kA + e]) *
-                   a.inv_dx[1];
-        cadv2[e] = (VK == 0 ? a.u[2] : P[(2 * 2 + 0) * nm + ig] + P[(2 * 2 + 1) * nm + jA + e]) *
-                   a.inv_dx[2];
-#endif
       }
       const int cq = (ph + M) % Q;
       double acc[4];
@@ -750,14 +662,7 @@ __global__ void __launch_bounds__(kV3Block, kV3Threads <= 128 ? 2 : 1) stencil_v
       }
       // axis 1: rows jl - m and jl + 1 + m are loaded once and serve both rows;
       // a second accumulator per point (8 independent DFMA chains per thread)
-#ifndef MR_V3_SPLIT
-#define MR_V3_SPLIT 0  // measured: 2 accumulators per point 4% slower
-#endif
-#if MR_V3_SPLIT
-      double acc1[4] = {0.0, 0.0, 0.0, 0.0};
-#else
       double (&acc1)[4] = acc;
-#endif
       double ru0 = qv[2][cq], ru1 = qv[3][cq];  // row jl + 1 (for m = 1: row jl + m)
       double pd0 = qv[0][cq], pd1 = qv[1][cq];  // row jl     (for m = 1: row jl + 1 - m)
 #pragma unroll
@@ -783,25 +688,14 @@ __global__ void __launch_bounds__(kV3Block, kV3Threads <= 128 ? 2 : 1) stencil_v
       for (int e = 0; e < 2; ++e) {
         double* o = orow + (size_t)e * n2;
         *reinterpret_cast<double2*>(o) =
-#if MR_V3_SPLIT
-            make_double2(acc[2 * e] + acc1[2 * e], acc[2 * e + 1] + acc1[2 * e + 1]);
-#else
             make_double2(acc[2 * e], acc[2 * e + 1]);
-#endif
       }
       orow += plane;
-#if MR_V3_MBAR
       __syncwarp();
       if (tx == 0) mbar_arrive(empty + (unsigned)t % R);  // this warp is done with plane i
-#if MR_V3_LATE_ISSUE
       issue_to(i + M + PF, s_iss);  // waits for the other warps to finish plane i - 1
-#endif
-#endif
     }
   }
-#if !MR_V3_MBAR
-  cp_async_wait<0>();
-#endif
 }
 
 // halo planes: send_lo = first g planes, send_hi = last g planes, per component

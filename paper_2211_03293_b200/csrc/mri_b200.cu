@@ -2087,25 +2087,6 @@ int mr_fast_chemistry(mr_ctx* c, int S, int R, double rho, const double* species
       return set_err(c, MR_CONTRACT, "mechanism too large for the chemistry kernel's shared memory");
     P.rc = rcz;
     P.nchunk = nch;
-    {  // balanced component -> (warp, slot) assignment (LPT greedy, SPL slots per warp)
-      const int NW = lay.NW, SPL = lay.SPL;
-      std::vector<int> order(S + 1);
-      std::vector<double> cost(S + 1, 0.0);
-      for (int k = 0; k < S; ++k) cost[k] = 16.0 + (double)(cnt[k + 1] - cnt[k]);
-      for (int k = 0; k <= S; ++k) order[k] = k;
-      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cost[x] > cost[y]; });
-      std::vector<double> load(NW, 0.0);
-      std::vector<int> used(NW, 0);
-      for (int i = 0; i < MR_CHEM_MAXS; ++i) P.perm[i] = 255;
-      for (int k : order) {
-        int best = -1;
-        for (int w2 = 0; w2 < NW; ++w2)
-          if (used[w2] < SPL && (best < 0 || load[w2] < load[best])) best = w2;
-        P.perm[best + NW * used[best]] = (unsigned char)k;
-        used[best]++;
-        load[best] += cost[k];
-      }
-    }
     std::vector<ChemRec> recs(R);
     for (int j = 0; j < R; ++j) {
       ChemRec& r = recs[j];
