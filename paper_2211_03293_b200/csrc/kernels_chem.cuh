@@ -18,8 +18,9 @@
 //     contributes RT/P, each present reactant P/RT), so a reaction is
 //     branch-free: kf = exp(lnA + beta lnT - Ea/RcT),
 //     q = kf (C_r1 C_r2 - (D'_p1 D'_p2)(E'_r1 E'_r2));
-//   * mechanism topology is pre-baked into shared-memory byte offsets
-//     (ChemParams::roff/poff/csr_ent), so there is no index decoding;
+//   * mechanism topology is pre-baked into shared-memory byte offsets (the
+//     ChemRec records and the production lists of the staged blob), so
+//     there is no index decoding;
 //   * rates of progress pass through a chunked shared buffer and are gathered
 //     per species in a fixed order (reaction ascending): bitwise deterministic
 //     and the oracle's summation order;
@@ -28,7 +29,10 @@
 //
 // Per RHS evaluation and cell: shared traffic 48 B gathered + 8 B stored per
 // reaction + 8 B per species-reaction incidence; fp64 work ~25 ops per
-// reaction.  Two blocks per SM overlap each other's barriers.
+// reaction.  The 54-component mechanisms run one
+// 1024-thread block per SM (32 warps x 2 components, 64 registers); the small
+// ones (NW = 4 / 8) several blocks per SM, which overlap each other's
+// barriers.  Per-evaluation scalars (tau) come precomputed in the arguments.
 #pragma once
 #include <cuda_runtime.h>
 
