@@ -229,6 +229,7 @@ struct mr_ctx {
   const double* host_in = nullptr;
   double* host_out = nullptr;  // ... and the result streams out during its last ops
   bool out_streamed = false;   // y_out was backed up to y_backup and is being written
+  bool pipeline_nccl = false;  // pipelined host step also on an NCCL rank (mr_debug_pipeline_nccl)
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[kHeadChunks + 1] = {};
   cudaStream_t comm_stream = nullptr;  // halo exchange overlapped with the interior stencil
@@ -1112,7 +1113,13 @@ int host_chunks(const mr_ctx* c, int* pb)
 bool pipeline_ok(const mr_ctx* c, const Plan& plan)
 {
   int pb[kHeadChunks + 1];
-  if (c->comm || c->in_domain || c->profile || c->fast_kind != FK_CHEM ||
+  // Not on NCCL ranks: the chunked schedule works there (the end chunks wait
+  // for the exchanged ghosts; tests/test_gpu_nccl.py with MR_PIPELINE_NCCL),
+  // but through the one-GPU loopback communicator it measured no better than
+  // the plain copies (705-744 vs 712 ms per slab step, the exchange kernels
+  // queue behind the chemistry), so ranks keep the plain upload/download until
+  // it can be measured on the 8-GPU box.  Not the in-process domains either.
+  if ((c->comm && !c->pipeline_nccl) || c->in_domain || c->profile || c->fast_kind != FK_CHEM ||
       c->slow_kind != SK_STENCIL || c->imex || host_chunks(c, pb) < 3 || plan.ops.size() < 2)
     return false;
   return stencil_plane_ranges(stencil_args(c, c->y_state, nullptr, nullptr, nullptr));
@@ -1155,9 +1162,39 @@ cudaError_t copy_chunk(mr_ctx* c, double* dst, const double* src, const int* pb,
                            kind, c->copy_stream);
 }
 
+// Ghost planes of a chunked slow evaluation of `y`: the first and last M
+// planes packed on `st`; on an NCCL rank they are then exchanged with the
+// neighbours on the comm stream (ev_halo marks their arrival), on a single
+// periodic slab the packed planes are the ghosts themselves.
+int chunk_halos(mr_ctx* c, const double* y, cudaStream_t st, StencilArgs& sa)
+{
+  MR_CUDA_TRY(c, launch_halo_pack(y, c->send_lo, c->send_hi, c->ncomp, c->n0l, c->plane, c->M, st));
+  c->launches++;
+  if (!c->comm) {
+    sa.halo_lo = c->send_hi;
+    sa.halo_hi = c->send_lo;
+    return MR_OK;
+  }
+  if (!c->comm_stream) {
+    MR_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    MR_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming));
+    MR_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+  }
+  MR_CUDA_TRY(c, cudaEventRecord(c->ev_pack, st));
+  MR_CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_pack, 0));
+  int rc = nccl_halo_exchange(c, c->comm_stream);
+  if (rc) return rc;
+  MR_CUDA_TRY(c, cudaEventRecord(c->ev_halo, c->comm_stream));
+  sa.halo_lo = c->recv_lo;
+  sa.halo_hi = c->recv_hi;
+  return MR_OK;
+}
+
 // Upload + ops[0] (SLOW 0) + ops[1] (CHAIN).  Chunks are copied in the order
-// K-1, 0, 1, ..., K-2 (the last chunk holds the periodic ghosts of the
-// first).  *nops = 2 when done, 0 when the plan does not start that way.
+// K-1, 0, 1, ..., K-2 (the end chunks hold the slab's ghost-source planes);
+// the stencil + chain of chunk q go as soon as chunks q-1..q+1 have landed --
+// on an NCCL rank the two end chunks last, after the exchanged ghosts.
+// *nops = 2 when done, 0 when the plan does not start that way.
 int head_upload(mr_ctx* c, const double* hin, const Plan& plan, double t, double H,
                 const ChemCfg& ccfg, cudaStream_t st, int* nops)
 {
@@ -1173,27 +1210,27 @@ int head_upload(mr_ctx* c, const double* hin, const Plan& plan, double t, double
   // the copies start after whatever the compute stream still does with y_state
   MR_CUDA_TRY(c, cudaEventRecord(c->ev_copy[kHeadChunks], st));
   MR_CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->ev_copy[kHeadChunks], 0));
+  auto pos = [&](int q) { return q == K - 1 ? 0 : q + 1; };  // place in the copy order
   for (int i = 0; i < K; ++i) {
     const int q = (i + K - 1) % K;  // K-1, 0, 1, ..., K-2
     MR_CUDA_TRY(c, copy_chunk(c, c->y_state, hin, pb, q, cudaMemcpyHostToDevice));
     MR_CUDA_TRY(c, cudaEventRecord(c->ev_copy[q], c->copy_stream));
   }
-  // periodic ghosts: the first and the last M planes (chunks 0 and K-1)
-  MR_CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_copy[0], 0));
-  MR_CUDA_TRY(c, launch_halo_pack(c->y_state, c->send_lo, c->send_hi, c->ncomp, c->n0l, c->plane,
-                                  c->M, st));
-  c->launches++;
-  StencilArgs sa = stencil_args(c, c->y_state, c->slots[plan.slot_of[0]], c->send_hi, c->send_lo);
+  StencilArgs sa = stencil_args(c, c->y_state, c->slots[plan.slot_of[0]], nullptr, nullptr);
+  MR_CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_copy[0], 0));  // chunks K-1 and 0
+  rc = chunk_halos(c, c->y_state, st, sa);
+  if (rc) return rc;
   const Op& o = plan.ops[1];
   ChainArgs a;
   fill_chain_args(c, o, plan, t, H, c->y_state, a);
   const NvtxRange r0("slow f_E", 0, -1);
   const NvtxRange r1("fast IVP chain", o.stages.front(), o.stages.back());
-  for (int q = 0; q < K; ++q) {
-    // chunks q - 1, q and q + 1 (the ghosts of chunks 0 and K-1 are packed);
-    // the copy stream is in order K-1, 0, 1, ..., K-2, so one event covers
-    // all three: chunk q + 1's, or chunk K-2's for the last two chunks
-    MR_CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_copy[q + 1 <= K - 2 ? q + 1 : K - 2], 0));
+  auto chunk = [&](int q) -> int {
+    // one copy event covers chunks q-1..q+1: the latest of them in copy order
+    int last = q;
+    if (q > 0 && pos(q - 1) > pos(last)) last = q - 1;
+    if (q + 1 < K && pos(q + 1) > pos(last)) last = q + 1;
+    MR_CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_copy[last], 0));
     sa.i_lo = pb[q];
     sa.i_hi = pb[q + 1];
     MR_CUDA_TRY(c, launch_stencil(sa, st));
@@ -1201,6 +1238,17 @@ int head_upload(mr_ctx* c, const double* hin, const Plan& plan, double t, double
     a.cell1 = (size_t)pb[q + 1] * c->plane;
     MR_CUDA_TRY(c, launch_chem_chain(ccfg, a, *c->chemP, st));
     c->launches += 2;
+    return MR_OK;
+  };
+  if (!c->comm) {
+    for (int q = 0; q < K; ++q)
+      if ((rc = chunk(q))) return rc;
+  } else {
+    for (int q = 1; q + 1 < K; ++q)
+      if ((rc = chunk(q))) return rc;
+    MR_CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
+    if ((rc = chunk(0))) return rc;
+    if ((rc = chunk(K - 1))) return rc;
   }
   *nops = 2;
   return MR_OK;
@@ -1225,8 +1273,10 @@ int tail_index(const Plan& plan, size_t first_op)
 // ops[L-2..L]: the last chain, slow evaluation and explicit update, chunk by
 // chunk, each finished chunk of the result streaming to hout.  Chain chunks in
 // the order K-1, 0, 1, ..., K-2; the stencil of chunk q once the chains of
-// q - 1..q + 1 are done; the (in-place) update of chunk q once the stencils
-// reading its planes (q - 1..q + 1) are done; then its download.
+// q-1..q+1 (or the ghosts, for the end chunks) are done; the in-place update
+// of chunk q once every stencil reading its planes (q-1..q+1) is done; then
+// its download.  An NCCL rank exchanges the ghosts once its end chunks are
+// final and runs the end chunks' stencils after they arrive.
 int tail_download(mr_ctx* c, const Plan& plan, int L, double t, double H, const ChemCfg& ccfg,
                   const double* yin, double* hout, cudaStream_t st)
 {
@@ -1239,62 +1289,70 @@ int tail_download(mr_ctx* c, const Plan& plan, int L, double t, double H, const 
   const Op& ou = plan.ops[L];
   ChainArgs a;
   fill_chain_args(c, oc, plan, t, H, yin, a);
-  StencilArgs sa = stencil_args(c, c->y_work, c->slots[plan.slot_of[os.stage]], c->send_hi,
-                                c->send_lo);
+  StencilArgs sa = stencil_args(c, c->y_work, c->slots[plan.slot_of[os.stage]], nullptr, nullptr);
   ChainStageDev sd;
   fill_chain_stage(c, ou.stage, t, H, plan, sd);
   const NvtxRange r0("fast IVP chain", oc.stages.front(), oc.stages.back());
   const NvtxRange r1("slow f_E", os.stage, -1);
   const NvtxRange r2("explicit update", ou.stage, -1);
-  auto chain = [&](int q) -> int {
+  std::vector<char> chained(K, 0), stenciled(K, 0), updated(K, 0);
+  bool ghosts = false;
+  auto stencil_ready = [&](int q) {
+    return chained[q] && (q == 0 ? ghosts : chained[q - 1] != 0) &&
+           (q == K - 1 ? ghosts : chained[q + 1] != 0);
+  };
+  auto update_ready = [&](int q) {
+    return stenciled[q] && (q == 0 || stenciled[q - 1]) && (q == K - 1 || stenciled[q + 1]);
+  };
+  auto advance = [&]() -> int {  // everything whose inputs are enqueued
+    for (int q = 0; q < K; ++q)
+      if (!stenciled[q] && stencil_ready(q)) {
+        sa.i_lo = pb[q];
+        sa.i_hi = pb[q + 1];
+        MR_CUDA_TRY(c, launch_stencil(sa, st));
+        c->launches++;
+        stenciled[q] = 1;
+      }
+    for (int q = 0; q < K; ++q)
+      if (!updated[q] && update_ready(q)) {
+        const size_t off = (size_t)pb[q] * c->plane;
+        const double* f[MR_MAXREF];
+        for (int r = 0; r < sd.nref; ++r) f[r] = c->slots[sd.ref_slot[r]] + off;
+        MR_CUDA_TRY(c, launch_update_rows(c->y_work + off, c->y_work + off, sd.nref, f, sd.coef[0],
+                                          (size_t)(pb[q + 1] - pb[q]) * c->plane, c->ncomp,
+                                          c->ncell, ou.stage, c->d_fail, st));
+        c->launches++;
+        MR_CUDA_TRY(c, cudaEventRecord(c->ev_copy[q], st));
+        MR_CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->ev_copy[q], 0));
+        MR_CUDA_TRY(c, copy_chunk(c, hout, c->y_work, pb, q, cudaMemcpyDeviceToHost));
+        updated[q] = 1;
+      }
+    return MR_OK;
+  };
+  for (int i = 0; i < K; ++i) {
+    const int q = (i + K - 1) % K;  // K-1, 0, 1, ..., K-2
     a.cell0 = (size_t)pb[q] * c->plane;
     a.cell1 = (size_t)pb[q + 1] * c->plane;
     MR_CUDA_TRY(c, launch_chem_chain(ccfg, a, *c->chemP, st));
     c->launches++;
-    return MR_OK;
-  };
-  auto stencil = [&](int q) -> int {
-    sa.i_lo = pb[q];
-    sa.i_hi = pb[q + 1];
-    MR_CUDA_TRY(c, launch_stencil(sa, st));
-    c->launches++;
-    return MR_OK;
-  };
-  auto update_out = [&](int q) -> int {
-    const size_t off = (size_t)pb[q] * c->plane;
-    const double* f[MR_MAXREF];
-    for (int r = 0; r < sd.nref; ++r) f[r] = c->slots[sd.ref_slot[r]] + off;
-    MR_CUDA_TRY(c, launch_update_rows(c->y_work + off, c->y_work + off, sd.nref, f, sd.coef[0],
-                                      (size_t)(pb[q + 1] - pb[q]) * c->plane, c->ncomp, c->ncell,
-                                      ou.stage, c->d_fail, st));
-    c->launches++;
-    MR_CUDA_TRY(c, cudaEventRecord(c->ev_copy[q], st));
-    MR_CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->ev_copy[q], 0));
-    MR_CUDA_TRY(c, copy_chunk(c, hout, c->y_work, pb, q, cudaMemcpyDeviceToHost));
-    return MR_OK;
-  };
-#define MR_TAIL(x)           \
-  do {                       \
-    const int rc_ = (x);     \
-    if (rc_) return rc_;     \
-  } while (0)
-  MR_TAIL(chain(K - 1));
-  MR_TAIL(chain(0));
-  // periodic ghosts of the last slow evaluation: chunks 0 and K-1 are final
-  MR_CUDA_TRY(c, launch_halo_pack(c->y_work, c->send_lo, c->send_hi, c->ncomp, c->n0l, c->plane,
-                                  c->M, st));
-  c->launches++;
-  for (int p = 1; p <= K - 2; ++p) {
-    MR_TAIL(chain(p));
-    MR_TAIL(stencil(p - 1));
-    if (p >= 2) MR_TAIL(update_out(p - 2));
+    chained[q] = 1;
+    if (q == 0) {  // both end chunks are final: their ghost-source planes go out
+      rc = chunk_halos(c, c->y_work, st, sa);
+      if (rc) return rc;
+      ghosts = !c->comm;
+    }
+    if ((rc = advance())) return rc;
   }
-  MR_TAIL(stencil(K - 2));
-  MR_TAIL(update_out(K - 3));
-  MR_TAIL(stencil(K - 1));
-  MR_TAIL(update_out(K - 2));
-  MR_TAIL(update_out(K - 1));
-#undef MR_TAIL
+  if (c->comm) {
+    // the exchanged ghosts, waited for only after the last chain chunk: the
+    // exchange kernels find SMs between the chain launches, and an earlier
+    // wait was measured to stall the compute stream (slab 1/8: 723 vs 705 ms)
+    MR_CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
+    ghosts = true;
+    if ((rc = advance())) return rc;
+  }
+  for (int q = 0; q < K; ++q)
+    if (!updated[q]) return set_err(c, MR_CUDA, "tail_download: chunk schedule incomplete");
   return MR_OK;
 }
 
@@ -3798,6 +3856,15 @@ int mr_debug_vector_bench(mr_ctx* c, double* out, int maxn)
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   return q;
+}
+
+// Debug (not part of include/mri_b200.h): let the pipelined host-buffer step
+// run on an NCCL rank (off by default, see pipeline_ok)
+int mr_debug_pipeline_nccl(mr_ctx* c, int on)
+{
+  if (!c) return MR_CONTRACT;
+  c->pipeline_nccl = on != 0;
+  return MR_OK;
 }
 
 // Debug (not part of include/mri_b200.h): chemistry phase cycles of an

@@ -93,3 +93,33 @@ def test_bench_nccl_self_line():
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert "one-rank NCCL path" in line["config"]["parallelism"]
     assert line["value"] > 0 and line["gpu_launches"] > 0
+
+
+@pytest.mark.parametrize("pipelined", [False, True])
+@pytest.mark.parametrize("name", ["C4", "C3"])
+def test_nccl_self_host_step_bitwise(monkeypatch, name, pipelined):
+    """The host-buffer step of an NCCL rank at 64^3 -- plain copies (the
+    default on ranks) and the chunk-pipelined schedule in which the end
+    chunks' slow evaluations wait for the exchanged ghosts (enabled through
+    the debug switch) -- bitwise the plain device step, counters equal; a
+    failing host step leaves y_out untouched."""
+    import ctypes as C
+    import torch
+    plain, nccl, cfg, y0 = _pair(monkeypatch, name, 64, dict(CONFIGS[name]))
+    f = P.lib().mr_debug_pipeline_nccl
+    f.argtypes = [C.c_void_p, C.c_int]
+    assert f(nccl.h, int(pipelined)) == 0
+    H = cfg["H"]
+    c_a = plain.mri_step(0.0, H)
+    y_in = torch.from_numpy(y0.copy()).pin_memory().numpy()
+    y_out = torch.zeros(y0.size, dtype=torch.float64).pin_memory().numpy()
+    c_b = nccl.counters()
+    nccl.mri_step_host(0.0, H, y_in, y_out, c_b)
+    assert np.array_equal(c_a, c_b)
+    assert np.array_equal(plain.download(), y_out)
+    bad = y_in.copy()
+    bad[-3] = np.nan
+    y_out[:] = 7.0
+    with pytest.raises(P.IntegrationError):
+        nccl.mri_step_host(0.0, H, bad, y_out)
+    assert np.all(y_out == 7.0)
