@@ -512,7 +512,9 @@ class Context:
     def mrsdc_load(self, scheme, sweeps):
         """Load a flattened MRSDC scheme (mrsdc_scheme(), or the reference's
         build_scheme) for mrsdc_integrate."""
-        sc = {k: np.ascontiguousarray(v) for k, v in scheme.items() if k not in ("X", "Y", "n_fine")}
+        ints = ("coarse_of_fine", "coarse_index_of_fine", "application_offset")
+        sc = {k: np.ascontiguousarray(v, dtype=np.int32 if k in ints else np.float64)
+              for k, v in scheme.items() if k not in ("X", "Y", "n_fine")}
         self._check(self.L.mr_mrsdc_load(
             self.h, scheme["X"], scheme["Y"], scheme["n_fine"], sweeps,
             _p(sc["coarse_nodes"]), _p(sc["fine_nodes"]), _p(sc["coarse_of_fine"], _ip),

@@ -3497,7 +3497,7 @@ int mr_mrsdc_load(mr_ctx* c, int X, int Y, int n_fine, int n_sweeps, const doubl
       !coarse_nodes || !fine_nodes || !coarse_of_fine || !coarse_index_of_fine || !fine_row ||
       !application_offset || !coarse_row)
     return set_err(c, MR_CONTRACT, "mr_mrsdc_load: bad scheme");
-  auto& M = c->mrsdc;
+  mr_ctx::SdcScheme M;  // validated before it replaces the loaded scheme
   M.X = X;
   M.Y = Y;
   M.n_fine = n_fine;
@@ -3516,6 +3516,7 @@ int mr_mrsdc_load(mr_ctx* c, int X, int Y, int n_fine, int n_sweeps, const doubl
     if (M.application_offset[q] < 0 || M.application_offset[q] + Y > n_fine)
       return set_err(c, MR_CONTRACT, "mr_mrsdc_load: application offset out of range");
   M.loaded = true;
+  c->mrsdc = std::move(M);
   return MR_OK;
 }
 

@@ -163,3 +163,17 @@ def test_contract_errors():
     ctx.mrsdc_build(3, 3, 1, 1)
     with pytest.raises(P.ContractError):
         ctx.mrsdc_integrate(1.0, 0.5, 0.1)  # tf must exceed t0
+    # a rejected load leaves the loaded scheme in place; int64 arrays are accepted
+    bad = P.mrsdc_scheme(3, 3, 2)
+    bad["application_offset"] = np.full(bad["n_fine"] - 1, 99, dtype=np.int64)
+    with pytest.raises(P.ContractError):
+        ctx.mrsdc_load(bad, 2)
+    good = {k: (v.astype(np.int64) if isinstance(v, np.ndarray) and v.dtype == np.int32 else v)
+            for k, v in P.mrsdc_scheme(3, 3, 1).items()}
+    a, b = lin_ctx(), lin_ctx()
+    a.mrsdc_build(3, 3, 1, 1)
+    b.mrsdc_load(good, 1)
+    ca, cb = a.mrsdc_integrate(0.0, 0.3, 0.1), b.mrsdc_integrate(0.0, 0.3, 0.1)
+    assert np.array_equal(a.download(), b.download()) and np.array_equal(ca, cb)
+    ctx.upload(np.asarray(Y0_LIN, dtype=np.float64))
+    ctx.mrsdc_integrate(0.0, 0.3, 0.1)  # the (3, 3, 1) scheme is still loaded
