@@ -321,9 +321,13 @@ def run_ours(args):
         e1.synchronize()
         barrier()
         ems = max_over_ranks(e0.elapsed_time(e1))
+        # bytes the host-buffer call actually moved per step (the pipelined
+        # step also saves y_out to the device, so H2D is twice the state)
+        h2d, d2h = ctx.last_host_step_bytes()
         e2e = {"value": ncell_job * e_steps / (ems * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": 8 * dof * world, "d2h_bytes_per_step": 8 * dof * world,
-               "steps": e_steps, "ms_per_step": ems / e_steps}
+               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+               "input_bytes_per_step": 8 * dof * world, "steps": e_steps,
+               "ms_per_step": ems / e_steps}
 
     # ---------------- CPU baseline (rank 0, N = 1 only) ----------------
     cpu = None

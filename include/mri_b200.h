@@ -171,6 +171,9 @@ int mr_mri_step_wait(mr_ctx* ctx, uint64_t* counters, int* fail_stage);
  * written back) and the device state is y_in. */
 int mr_mri_step_host(mr_ctx* ctx, double t, double H, const double* y_in, double* y_out,
                      uint64_t* counters, int* fail_stage);
+/* Host<->device bytes the last mr_mri_step_host moved (the pipelined step also
+ * saves y_out to the device: 2 x state H2D). */
+int mr_last_host_step_bytes(const mr_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 /* ark_imex_step / ark_imex_integrate (proj/src/mri.cpp:437-557): the
  * single-rate ARK4(3)6L[2]SA IMEX pair (butcher.cpp:362-427) on the same
  * plugins -- explicit part f_fast + f_explicit, implicit f_implicit solved

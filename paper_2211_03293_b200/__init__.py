@@ -119,6 +119,7 @@ def lib():
         "mr_mri_integrate": (C.c_int, [vp, C.c_double, C.c_double, C.c_double, _u64p, _ip]),
         "mr_mri_step_host": (C.c_int, [vp, C.c_double, C.c_double, _dp, _dp, _u64p, _ip]),
         "mr_last_failure": (C.c_int, [vp, _ip, _ip, _ip]),
+        "mr_last_host_step_bytes": (C.c_int, [vp, _u64p, _u64p]),
         "mr_fast_rhs": (C.c_int, [vp, C.c_double, _dp, _dp]),
         "mr_slow_rhs": (C.c_int, [vp, C.c_double, _dp, _dp]),
         "mr_wrms_norm": (C.c_int, [vp, C.c_void_p, C.c_void_p, C.c_size_t, _dp]),
@@ -529,6 +530,12 @@ class Context:
         rc = self.L.mr_mrsdc_integrate(self.h, t0, tf, H, _p(cnt, _u64p), C.byref(stage))
         self._check(rc, stage.value)
         return cnt
+
+    def last_host_step_bytes(self):
+        """(H2D, D2H) bytes the last mri_step_host moved over PCIe."""
+        a, b = C.c_uint64(), C.c_uint64()
+        self._check(self.L.mr_last_host_step_bytes(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def last_failure(self):
         a, b, c = C.c_int(), C.c_int(), C.c_int()

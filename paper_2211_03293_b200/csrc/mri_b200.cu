@@ -230,6 +230,7 @@ struct mr_ctx {
   double* host_out = nullptr;  // ... and the result streams out during its last ops
   bool out_streamed = false;   // y_out was backed up to y_backup and is being written
   bool pipeline_nccl = false;  // pipelined host step also on an NCCL rank (mr_debug_pipeline_nccl)
+  uint64_t host_h2d = 0, host_d2h = 0;  // bytes the last host-buffer step moved
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[kHeadChunks + 1] = {};
   cudaStream_t comm_stream = nullptr;  // halo exchange overlapped with the interior stencil
@@ -2799,25 +2800,45 @@ int mr_mri_step_host(mr_ctx* c, double t, double H, const double* y_in, double* 
   int rc = ensure_state(c);
   if (rc) return rc;
   // the step itself moves the data (domain_step: head_upload / tail_download)
+  const uint64_t bytes = (uint64_t)c->dof * sizeof(double);
   c->host_in = y_in;
   c->host_out = y_out;
   c->out_streamed = false;
+  c->host_h2d = bytes;  // y_in
+  c->host_d2h = 0;
   rc = mr_mri_step(c, t, H, counters, fail_stage);
   c->host_in = nullptr;
   c->host_out = nullptr;
-  if (c->out_streamed) {  // y_out was written by the step's last ops
+  if (c->out_streamed) {  // y_out was saved (H2D) and written by the step's last ops
     c->out_streamed = false;
+    c->host_h2d += bytes;
+    c->host_d2h = bytes;
     MR_CUDA_TRY(c, cudaStreamSynchronize(c->copy_stream));
     if (rc) {  // no partial result: the caller's buffer as it was
       cudaMemcpy(y_out, c->y_backup, c->dof * sizeof(double), cudaMemcpyDeviceToHost);
+      c->host_d2h += bytes;
       return rc;
     }
     return MR_OK;
   }
   if (rc) return rc;
+  c->host_d2h = bytes;
   MR_CUDA_TRY(c, cudaMemcpyAsync(y_out, c->y_state, c->dof * sizeof(double),
                                  cudaMemcpyDeviceToHost, c->stream));
   MR_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MR_OK;
+}
+
+int mr_last_host_step_bytes(const mr_ctx* c, uint64_t* h2d, uint64_t* d2h)
+{
+  if (!c || !h2d || !d2h) return MR_CONTRACT;
+  uint64_t a = c->host_h2d, b = c->host_d2h;
+  for (const mr_ctx* sl : c->slabs) {
+    a += sl->host_h2d;
+    b += sl->host_d2h;
+  }
+  *h2d = a;
+  *d2h = b;
   return MR_OK;
 }
 

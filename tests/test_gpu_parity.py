@@ -466,6 +466,9 @@ def test_host_buffer_step_equals_device_step(name, n):
     host.mri_step_host(0.0, cfg["H"], y_in, y_out, c_host)
     assert np.array_equal(c_host, c_dev)
     assert np.array_equal(y_out, ref)
+    # PCIe bytes: the state each way, plus the saved y_out when pipelined (n >= 64)
+    state = 8 * y0.size
+    assert host.last_host_step_bytes() == ((2 if n >= 64 else 1) * state, state)
     y_pageable = np.zeros_like(y0)  # pageable destination: same result
     host.mri_step_host(0.0, cfg["H"], y0, y_pageable)
     assert np.array_equal(y_pageable, ref)
